@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 LLG step (BASELINE.json metric: LLG cell-updates/s and % of HBM
+roofline) on the 512x512x8 fp32 thin-film scaling point (BASELINE configs[2], the north
+star's target configuration; SP#3 material, random initial state, no applied field).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload ...]
+
+One process per GPU (torchrun for N > 1). The 512x512x8 grid fits one GPU, so N > 1 runs N
+independent replicas ("replicas only", scaling "weak"); time = max over ranks of the
+CUDA-event time of K steps; value = total cell-updates of all ranks / that time.
+--impl reference times the reference's own CPU solver (oracle/_ref: the reference sources
+compiled in place with the FFTW-API shim) on the host cores, rank 0 only.
+Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (nx, ny, nz, delta, a_ex, ms, hk, alpha, dt, precision)
+    "512x512x8_f32": (512, 512, 8, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5, "f32"),
+    "1024x1024x32_f32": (1024, 1024, 32, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5, "f32"),
+    "256x256x1_f32": (256, 256, 1, 3.0, 1.3e7, 800.0, 0.0, 0.5, 5e-6, "f32"),
+    "256x256x1_f64": (256, 256, 1, 3.0, 1.3e7, 800.0, 0.0, 0.5, 5e-6, "f64"),
+    "sp4_128x32x1_f64": (128, 32, 1, 3.90625, 1.3e7, 800.0, 0.0, 0.5, 5e-6, "f64"),
+}
+METRIC = "LLG cell-updates/s"
+UNIT = "cell-updates/s"
+
+
+def algorithmic_bytes(nx, ny, nz, w):
+    """SURVEY.md §8(d) canonical per-step bytes and the per-kernel split (one HBM read and
+    write per stage of the pruned r2c pipeline; tensor = 6 real octants)."""
+    n = nx * ny * nz
+    lx = 1 if nx == 1 else 1 << math.ceil(math.log2(2 * nx - 1))
+    ly = 1 if ny == 1 else 1 << math.ceil(math.log2(2 * ny - 1))
+    lz = 1 if nz == 1 else 1 << math.ceil(math.log2(2 * nz - 1))
+    xh = 1 if lx == 1 else lx // 2 + 1
+    yh = 1 if ly == 1 else ly // 2 + 1
+    zh = 1 if lz == 1 else lz // 2 + 1
+    half = 3 * xh * ny * nz * 2 * w          # live half-spectrum rows (complex)
+    padded = 3 * xh * ly * nz * 2 * w        # after the y-forward
+    tensor = 6 * xh * yh * zh * w
+    k = {"x_fwd": 3 * n * w + half, "x_inv": half + 3 * n * w, "llg": 9 * n * w}
+    if nz == 1:
+        k["y_mac"] = 2 * half + tensor
+    else:
+        k["y_fwd"] = half + padded
+        k["z_mac"] = 2 * padded + tensor
+        k["y_inv"] = padded + half
+    return sum(k.values()), k
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        load = [r for r in rows if r[2].isdigit() and int(r[2]) > 0] or rows
+        sm = [int(r[0]) for r in load if r[0].isdigit()]
+        mx = [int(r[1]) for r in rows if r[1].isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(load)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, v):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(world, v):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def random_state(nx, ny, nz, ms, dtype, seed=20240):
+    rng = np.random.default_rng(seed + nx)
+    v = rng.uniform(-1.0, 1.0, (3, nz, ny, nx))
+    v /= np.maximum(np.sqrt((v * v).sum(0)), 0.1)
+    return (ms * v).astype(dtype)
+
+
+def profile_summary(workload):
+    """ncu-derived DRAM traffic per launch of the dominant kernel, if committed."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(workload, {})
+    except Exception:
+        return {}
+
+
+def cpu_reference_time(wl, steps_max, budget_s, warmup=1):
+    """Reference Simulation<T>::step() (oracle/_ref) on the host cores, timed like
+    proj/src/benchmark.cpp:40-46 (steady clock, warm-up then measured steps)."""
+    from oracle import ref
+    nx, ny, nz, delta, a_ex, ms, hk, alpha, dt, prec = WORKLOADS[wl]
+    if not ref.available():
+        raise RuntimeError("oracle/_ref/libmmsim_ref.so missing (build with make -C oracle)")
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    P = ref.Problem(nx, ny, nz, delta, a_ex, ms, hk, alpha, dt)
+    t0 = time.perf_counter()
+    sim = ref.RefSimulation(P, prec, backend="parallel")
+    setup = time.perf_counter() - t0
+    sim.set_m(random_state(nx, ny, nz, ms, np.float64 if prec == "f64" else np.float32))
+    for _ in range(warmup):
+        sim.step(1)
+    done, t = 0, 0.0
+    while done < max(1, steps_max):
+        t1 = time.perf_counter()
+        sim.step(1)
+        t += time.perf_counter() - t1
+        done += 1
+        if t > budget_s:
+            break
+    n = nx * ny * nz
+    return {"value": n * done / t, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]),
+            "kind": "reference",
+            "sample": f"{done} full {nx}x{ny}x{nz} {prec} steps after {warmup} warm-up "
+                      f"(reference serial FFT + OpenMP field loops, FFTW-API shim; setup {setup:.1f}s "
+                      "excluded)",
+            "ms_per_step": 1e3 * t / done, "steps": done}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    wl = args.workload
+    nx, ny, nz, *_ , prec = WORKLOADS[wl]
+    c = cpu_reference_time(wl, args.steps, budget_s=float(os.environ.get("MMB_REF_BUDGET_S", "120")),
+                           warmup=min(args.warmup, 1))
+    line = {"metric": METRIC, "value": c["value"], "unit": UNIT, "n_gpus": world, "steps": c["steps"],
+            "warmup": min(args.warmup, 1), "ms_per_step": c["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": wl, "nx": nx, "ny": ny, "nz": nz, "parallelism": "host cores"},
+            "cpu_baseline": c,
+            "e2e": {"value": c["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args, world, rank, local):
+    from paper_1501_07293_b200 import (Grid, MaterialParams, Precision, ProblemSpec, make_simulation)
+    import torch
+    wl = args.workload
+    nx, ny, nz, delta, a_ex, ms, hk, alpha, dt, prec = WORKLOADS[wl]
+    dtype = np.float32 if prec == "f32" else np.float64
+    w = 4 if prec == "f32" else 8
+    n = nx * ny * nz
+    spec = ProblemSpec(name=wl, grid=Grid(nx, ny, nz, delta), material=MaterialParams(a_ex, ms, hk, alpha),
+                       dt=dt)
+    sim = make_simulation(spec, precision=Precision.f32 if prec == "f32" else Precision.f64, device=local)
+    m0 = random_state(nx, ny, nz, ms, dtype)
+    sim.set_magnetization(m0)
+
+    # ---- device-resident throughput (value)
+    sim.time_steps(max(3, args.warmup))
+    barrier(world)
+    with ClockSampler(local) as clk:
+        t_ms = sim.time_steps(args.steps)
+    t_ms = max_over_ranks(world, t_ms)
+    value = n * args.steps * world / (t_ms * 1e-3)
+    ms_step = t_ms / args.steps
+
+    # ---- per-kernel times (eager launches with events) for the roofline
+    prof = sim.profile_step(max(5, min(args.steps, 20)))
+    b_alg, kbytes = algorithmic_bytes(nx, ny, nz, w)
+    peak, peak_kind = load_peaks()
+    top = max(prof, key=prof.get)
+    achieved = kbytes[top] / (prof[top] * 1e-3) / 1e9
+    ps = profile_summary(wl)
+    traffic = ps.get(top, {}).get("dram_bytes") if ps else None
+    roof = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "alg_bytes": kbytes[top],
+            "kernel_ms": prof[top], "peak_kind": peak_kind,
+            "step": {"alg_bytes": b_alg, "achieved": b_alg / (ms_step * 1e-3) / 1e9,
+                     "frac": b_alg / (ms_step * 1e-3) / 1e9 / peak},
+            "kernels_ms": prof}
+
+    # ---- end to end through the public API with host buffers (pinned): per step
+    # H2D of M, one step, D2H of M
+    pin_in = torch.empty((3, nz, ny, nx), dtype=torch.float32 if prec == "f32" else torch.float64,
+                         pin_memory=True).numpy()
+    pin_out = torch.empty_like(torch.from_numpy(pin_in)).pin_memory().numpy()
+    pin_in[...] = m0
+    for _ in range(2):
+        sim.set_m_from(pin_in)
+        sim.step(1)
+        sim.get_m_into(pin_out)
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sim.set_m_from(pin_in)
+        sim.step(1)
+        sim.get_m_into(pin_out)
+    te = max_over_ranks(world, time.perf_counter() - t0)
+    e2e = {"value": n * args.steps * world / te, "unit": UNIT,
+           "h2d_bytes_per_step": 3 * n * w, "d2h_bytes_per_step": 3 * n * w,
+           "api": "mmb_set_m + mmb_step(1) + mmb_get_m per step (libmmb.so C-ABI via ctypes)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_reference_time(wl, 2, budget_s=20.0, warmup=1)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+                "config": {"workload": wl, "nx": nx, "ny": ny, "nz": nz, "delta_nm": delta,
+                           "material": "SP#3 (Ms=1000, A=1e-11 J/m, Hk=100, alpha=0.5)"
+                           if nz > 1 else "permalloy (Ms=800, A=1.3e-11 J/m)",
+                           "initial_state": "seeded random unit field",
+                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                           "l2": "per-step working set (spectrum scratch + M/H + tensor) > 126 MB L2; no flush",
+                           "cells": n},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": sim.launches_per_step() * args.steps,
+                "clocks": clk.summary(),
+                "device_bytes": sim.device_bytes()}
+        print(json.dumps(line), flush=True)
+    barrier(world)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="512x512x8_f32", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    world, rank, local = dist_setup() if args.impl == "b200" else (
+        int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    return run_b200(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

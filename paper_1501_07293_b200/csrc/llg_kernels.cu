@@ -1,0 +1,332 @@
+// llg_kernels.cu — fused local terms + explicit-Euler LLG update, reductions and the
+// one-time prism-sum tensor entries. Compiled with --fmad=false: every product and sum here
+// rounds separately, exactly like the reference's x86-64 (SSE2, no FMA) build, so given the
+// same H_demag the local part of H_eff and the updated M agree bitwise.
+#include <stdexcept>
+#include <string>
+
+#include "kernels.hpp"
+
+namespace mmb {
+
+namespace {
+
+constexpr int kLlgThreads = 256;
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 592; // 4 x 148 SMs; fixed so the reduction order is deterministic
+
+void check_launch() {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Exchange sum for one component, neighbour order -x,+x,-y,+y,-z,+z with Neumann skips
+// (proj/src/local_fields.cpp:27-39).
+template <typename T>
+__device__ __forceinline__ T exch_sum(const T* __restrict__ src, long long f, int i, int j, int k,
+                                      int nx, int ny, int nz, long long sy, long long sz) {
+    const T center = __ldg(src + f);
+    T sum = T(0);
+    if (i > 0) sum += __ldg(src + f - 1) - center;
+    if (i + 1 < nx) sum += __ldg(src + f + 1) - center;
+    if (j > 0) sum += __ldg(src + f - sy) - center;
+    if (j + 1 < ny) sum += __ldg(src + f + sy) - center;
+    if (k > 0) sum += __ldg(src + f - sz) - center;
+    if (k + 1 < nz) sum += __ldg(src + f + sz) - center;
+    return sum;
+}
+
+// K6: one thread per cell.
+//   H = H_demag; H += coeff * exch_sum (local_fields.cpp:39); Hx += (hk/ms) Mx
+//   (local_fields.hpp:28-31); H += applied (local_fields.hpp:43-55)
+//   T = M x H; dM = p1 T + p2 (M x T); M += dM (llg.cpp:82-93); max |T|^2 in fp64 (:89-90)
+//   mag = sqrt(Mx^2 + My^2 + Mz^2); M *= T(ms)/mag (vector_field.hpp:56-76)
+// MODE 1 writes H_eff instead (field assembly only).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kLlgThreads) k_llg(const T* __restrict__ m, const T* __restrict__ hd,
+                                                     T* __restrict__ out, Geom g, T coeff, T kan,
+                                                     StepCtl* ctl) {
+    const long long n = g.n;
+    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    const long long sy = nx, sz = static_cast<long long>(nx) * ny;
+    const T ax = static_cast<T>(ctl->field[0]);
+    const T ay = static_cast<T>(ctl->field[1]);
+    const T az = static_cast<T>(ctl->field[2]);
+    const T p1 = static_cast<T>(ctl->p1);
+    const T p2 = static_cast<T>(ctl->p2);
+    const T ms = static_cast<T>(ctl->ms);
+    const long long cur = ctl->cur_step;
+    if (MODE == 0 && blockIdx.x == 0 && threadIdx.x == 0) ctl->step = cur + 1;
+
+    double tmax = 0.0;
+    const long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (f < n) {
+        const int i = static_cast<int>(f % nx);
+        const long long r = f / nx;
+        const int j = static_cast<int>(r % ny);
+        const int k = static_cast<int>(r / ny);
+        const T* mxp = m;
+        const T* myp = m + n;
+        const T* mzp = m + 2 * n;
+        const T mx = __ldg(mxp + f), my = __ldg(myp + f), mz = __ldg(mzp + f);
+        T hx = __ldg(hd + f), hy = __ldg(hd + n + f), hz = __ldg(hd + 2 * n + f);
+        hx += coeff * exch_sum(mxp, f, i, j, k, nx, ny, nz, sy, sz);
+        hy += coeff * exch_sum(myp, f, i, j, k, nx, ny, nz, sy, sz);
+        hz += coeff * exch_sum(mzp, f, i, j, k, nx, ny, nz, sy, sz);
+        hx += kan * mx;
+        hx += ax;
+        hy += ay;
+        hz += az;
+        if constexpr (MODE == 1) {
+            out[f] = hx;
+            out[n + f] = hy;
+            out[2 * n + f] = hz;
+        } else {
+            const T tx = my * hz - mz * hy;
+            const T ty = mz * hx - mx * hz;
+            const T tz = mx * hy - my * hx;
+            const T dx = p1 * tx + p2 * (my * tz - mz * ty);
+            const T dy = p1 * ty + p2 * (mz * tx - mx * tz);
+            const T dz = p1 * tz + p2 * (mx * ty - my * tx);
+            tmax = double(tx) * tx + double(ty) * ty + double(tz) * tz;
+            T nxv = mx + dx, nyv = my + dy, nzv = mz + dz;
+            const T mag = sqrt(nxv * nxv + nyv * nyv + nzv * nzv);
+            if (mag == T(0)) {
+                atomicMin(&ctl->bad_key, (static_cast<unsigned long long>(cur) << 36) |
+                                             static_cast<unsigned long long>(f));
+            } else {
+                const T scale = ms / mag;
+                nxv *= scale;
+                nyv *= scale;
+                nzv *= scale;
+            }
+            out[f] = nxv;
+            out[n + f] = nyv;
+            out[2 * n + f] = nzv;
+        }
+    }
+    if constexpr (MODE == 0) {
+        __shared__ double red[kLlgThreads / 32];
+        tmax = warp_max(tmax);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = tmax;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double v = threadIdx.x < kLlgThreads / 32 ? red[threadIdx.x] : 0.0;
+            v = warp_max(v);
+            if (threadIdx.x == 0) atomicMax(&ctl->torque_sq_bits, __double_as_longlong(v));
+        }
+    }
+}
+
+// Block-partial fp64 sums of the three components in a fixed order.
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_sum3(const T* __restrict__ m, long long n,
+                                                      double* __restrict__ partial) {
+    double s[3] = {0.0, 0.0, 0.0};
+    for (long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; f < n;
+         f += static_cast<long long>(gridDim.x) * blockDim.x) {
+        s[0] += double(__ldg(m + f));
+        s[1] += double(__ldg(m + n + f));
+        s[2] += double(__ldg(m + 2 * n + f));
+    }
+    __shared__ double red[3][kRedThreads / 32];
+    for (int c = 0; c < 3; ++c) {
+        const double v = warp_sum(s[c]);
+        if ((threadIdx.x & 31) == 0) red[c][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double t = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) t += red[threadIdx.x][w];
+        partial[blockIdx.x * 3 + threadIdx.x] = t;
+    }
+}
+
+// Sums nblk x NV partials in block order (one warp per value).
+template <int NV>
+__global__ void k_final_sum(const double* __restrict__ partial, int nblk, double* __restrict__ out) {
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (c >= NV) return;
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += partial[b * NV + c];
+    s = warp_sum(s);
+    if (lane == 0) out[c] = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_torque_max(const T* __restrict__ m, const T* __restrict__ h,
+                                                            long long n, unsigned long long* out) {
+    double t = 0.0;
+    for (long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; f < n;
+         f += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const double mx = m[f], my = m[n + f], mz = m[2 * n + f];
+        const double hx = h[f], hy = h[n + f], hz = h[2 * n + f];
+        const double tx = my * hz - mz * hy;
+        const double ty = mz * hx - mx * hz;
+        const double tz = mx * hy - my * hx;
+        t = fmax(t, tx * tx + ty * ty + tz * tz);
+    }
+    __shared__ double red[kRedThreads / 32];
+    t = warp_max(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < kRedThreads / 32 ? red[threadIdx.x] : 0.0;
+        v = warp_max(v);
+        if (threadIdx.x == 0) atomicMax(out, __double_as_longlong(v));
+    }
+}
+
+// proj/src/energy.cpp:39-64 local density (anisotropy + demag + Zeeman) and the
+// forward-difference exchange bonds (:17-36), fp64.
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_energy(const T* __restrict__ m, const T* __restrict__ hd,
+                                                        Geom g, double ku_over_ms2,
+                                                        const StepCtl* ctl, double* __restrict__ partial) {
+    const long long n = g.n;
+    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    const double ex = ctl->field[0], ey = ctl->field[1], ez = ctl->field[2];
+    double loc = 0.0, bonds = 0.0;
+    for (long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; f < n;
+         f += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const double x = m[f], y = m[n + f], z = m[2 * n + f];
+        const double hx = hd[f], hy = hd[n + f], hz = hd[2 * n + f];
+        const double anis = ku_over_ms2 * (y * y + z * z);
+        const double demag = -0.5 * kMu0 * (hx * x + hy * y + hz * z);
+        const double zeeman = -kMu0 * (ex * x + ey * y + ez * z);
+        loc += anis + demag + zeeman;
+        const int i = static_cast<int>(f % nx);
+        const long long r = f / nx;
+        const int j = static_cast<int>(r % ny);
+        const int k = static_cast<int>(r / ny);
+        auto bond = [&](long long b) {
+            const double dx = double(m[b]) - x, dy = double(m[n + b]) - y, dz = double(m[2 * n + b]) - z;
+            return dx * dx + dy * dy + dz * dz;
+        };
+        if (i + 1 < nx) bonds += bond(f + 1);
+        if (j + 1 < ny) bonds += bond(f + nx);
+        if (k + 1 < nz) bonds += bond(f + static_cast<long long>(nx) * ny);
+    }
+    __shared__ double red[2][kRedThreads / 32];
+    loc = warp_sum(loc);
+    bonds = warp_sum(bonds);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = loc;
+        red[1][threadIdx.x >> 5] = bonds;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        double t = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) t += red[threadIdx.x][w];
+        partial[blockIdx.x * 2 + threadIdx.x] = t;
+    }
+}
+
+// K0: the eight-corner prism sums (proj/src/demag_tensor.cpp:9-43) in fp64 for offsets
+// (I, J, K) >= 0; other octants follow by parity. E is [6][nz][ny][nx].
+__global__ void k_tensor_octant(double* __restrict__ E, int nx, int ny, int nz, double delta) {
+    const long long cnt = static_cast<long long>(nx) * ny * nz;
+    const long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (f >= cnt) return;
+    const int I = static_cast<int>(f % nx);
+    const int J = static_cast<int>((f / nx) % ny);
+    const int K = static_cast<int>(f / (static_cast<long long>(nx) * ny));
+    double xx = 0, xy = 0, xz = 0, yy = 0, yz = 0, zz = 0;
+#pragma unroll
+    for (int i = 0; i <= 1; ++i)
+#pragma unroll
+        for (int j = 0; j <= 1; ++j)
+#pragma unroll
+            for (int k = 0; k <= 1; ++k) {
+                const double sign = ((i + j + k) & 1) ? -1.0 : 1.0;
+                const double x = I + i - 0.5;
+                const double y = J + j - 0.5;
+                const double z = K + k - 0.5;
+                const double r = delta * sqrt(x * x + y * y + z * z);
+                xx += sign * atan(z * y * delta / (r * x));
+                yy += sign * atan(x * z * delta / (r * y));
+                zz += sign * atan(y * x * delta / (r * z));
+                xy += sign * log(z * delta + r);
+                xz += sign * log(y * delta + r);
+                yz += sign * log(x * delta + r);
+            }
+    const double p = 1.0 / (4.0 * 3.14159265358979323846);
+    E[0 * cnt + f] = xx * p;
+    E[1 * cnt + f] = xy * -p;
+    E[2 * cnt + f] = xz * -p;
+    E[3 * cnt + f] = yy * p;
+    E[4 * cnt + f] = yz * -p;
+    E[5 * cnt + f] = zz * p;
+}
+
+} // namespace
+
+int reduce_blocks(long long n) {
+    const long long b = (n + kRedThreads - 1) / kRedThreads;
+    return static_cast<int>(b < kRedBlocks ? (b < 1 ? 1 : b) : kRedBlocks);
+}
+
+template <typename T>
+void launch_llg(int mode, const T* m, const T* hd, T* out, const Geom& g, double exch_coeff,
+                double aniso_coeff, StepCtl* ctl, cudaStream_t stream) {
+    const unsigned blocks = static_cast<unsigned>((g.n + kLlgThreads - 1) / kLlgThreads);
+    const T coeff = static_cast<T>(exch_coeff), kan = static_cast<T>(aniso_coeff);
+    if (mode == 0) k_llg<T, 0><<<blocks, kLlgThreads, 0, stream>>>(m, hd, out, g, coeff, kan, ctl);
+    else k_llg<T, 1><<<blocks, kLlgThreads, 0, stream>>>(m, hd, out, g, coeff, kan, ctl);
+    check_launch();
+}
+
+template <typename T>
+void launch_sum3(const T* m, long long n, double* partial, double* out, cudaStream_t stream) {
+    const int nb = reduce_blocks(n);
+    k_sum3<T><<<nb, kRedThreads, 0, stream>>>(m, n, partial);
+    k_final_sum<3><<<1, 96, 0, stream>>>(partial, nb, out);
+    check_launch();
+}
+
+template <typename T>
+void launch_torque_max(const T* m, const T* h, long long n, unsigned long long* out_bits,
+                       cudaStream_t stream) {
+    cudaMemsetAsync(out_bits, 0, sizeof(unsigned long long), stream);
+    k_torque_max<T><<<reduce_blocks(n), kRedThreads, 0, stream>>>(m, h, n, out_bits);
+    check_launch();
+}
+
+template <typename T>
+void launch_energy(const T* m, const T* hd, const Geom& g, double ku_over_ms2, const StepCtl* ctl,
+                   double* partial, double* out, cudaStream_t stream) {
+    const int nb = reduce_blocks(g.n);
+    k_energy<T><<<nb, kRedThreads, 0, stream>>>(m, hd, g, ku_over_ms2, ctl, partial);
+    k_final_sum<2><<<1, 64, 0, stream>>>(partial, nb, out);
+    check_launch();
+}
+
+void launch_tensor_octant(double* E, int nx, int ny, int nz, double delta, cudaStream_t stream) {
+    const long long cnt = static_cast<long long>(nx) * ny * nz;
+    k_tensor_octant<<<static_cast<unsigned>((cnt + 127) / 128), 128, 0, stream>>>(E, nx, ny, nz, delta);
+    check_launch();
+}
+
+#define MMB_INST(T)                                                                                 \
+    template void launch_llg<T>(int, const T*, const T*, T*, const Geom&, double, double, StepCtl*, \
+                                cudaStream_t);                                                     \
+    template void launch_sum3<T>(const T*, long long, double*, double*, cudaStream_t);              \
+    template void launch_torque_max<T>(const T*, const T*, long long, unsigned long long*,          \
+                                       cudaStream_t);                                              \
+    template void launch_energy<T>(const T*, const T*, const Geom&, double, const StepCtl*,         \
+                                   double*, double*, cudaStream_t);
+MMB_INST(float)
+MMB_INST(double)
+
+} // namespace mmb

@@ -1,0 +1,715 @@
+// solver.cu — host side of the B200 LLG step: device buffers, the per-step launch sequence,
+// CUDA-graph replay, synchronising queries, and the mmb.h C-ABI.
+//
+// Mirrors mmsim::Simulation<T> (proj/include/mmsim/llg.hpp:78-115, proj/src/llg.cpp):
+// same construction (material validation, uniform initial state, tensor precompute),
+// same step semantics (schedule at the 0-based step before increment, sticky alpha
+// override, demag -> exchange -> anisotropy -> applied accumulation, Euler update with
+// fp64 torque max, renormalisation), same run() cadence/stop rules and the same error
+// contract (exceptions mapped to status codes as proj/src/capi.cpp:31-58 does).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mmb.h"
+#include "kernels.hpp"
+
+namespace mmb {
+
+struct numerical_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct cuda_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+static void ck(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) throw std::bad_alloc();
+    if (e != cudaSuccess) throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static int pow2_at_least(int v) {
+    int l = 1;
+    while (l < v) l <<= 1;
+    return l;
+}
+static int ilog2(int v) {
+    int r = 0;
+    while ((1 << r) < v) ++r;
+    return r;
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        n = count;
+        if (count) ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+class SolverBase {
+public:
+    virtual ~SolverBase() = default;
+    virtual int precision() const = 0;
+    virtual void set_m(const void*, const void*, const void*) = 0;
+    virtual void get_m(void*, void*, void*) = 0;
+    virtual void step(long long n) = 0;
+    virtual long long step_index() const = 0;
+    virtual void average(double* out) = 0;
+    virtual double energy() = 0;
+    virtual double max_torque() = 0;
+    virtual double last_torque_sq() = 0;
+    virtual long long run(long long steps, long long cadence, double stop_torque,
+                          mmb_record_fn fn, void* user) = 0;
+    virtual void synchronize() = 0;
+    virtual void effective_field(void*, void*, void*) = 0;
+    virtual void demag_field(const void*, const void*, const void*, void*, void*, void*) = 0;
+    virtual void tensor_octant(double*) = 0;
+    virtual void upload_tensor_octant(const double*) = 0;
+    virtual float time_steps(long long n) = 0;
+    virtual int profile_step(long long n, float* ms, int maxk, std::string& names) = 0;
+    virtual int launches_per_step() const = 0;
+    virtual size_t device_bytes() const = 0;
+};
+
+template <typename T>
+class Solver final : public SolverBase {
+public:
+    Solver(const mmb_desc& d, const mmb_stage* stages, int nstages) : d_(d) {
+        if (d.nx < 1 || d.ny < 1 || d.nz < 1) throw std::invalid_argument("Grid: cell counts must be >= 1");
+        if (!(d.delta > 0.0)) throw std::invalid_argument("Grid: cell edge length must be > 0");
+        // MaterialParams::validate (proj/include/mmsim/material.hpp:17-22)
+        if (!(d.ms > 0.0)) throw std::invalid_argument("MaterialParams: ms must be > 0");
+        if (d.a_ex < 0.0) throw std::invalid_argument("MaterialParams: a_ex must be >= 0");
+        if (d.hk < 0.0) throw std::invalid_argument("MaterialParams: hk must be >= 0");
+        if (!(d.alpha > 0.0)) throw std::invalid_argument("MaterialParams: alpha must be > 0");
+        set_schedule(stages, nstages);
+
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw cuda_error("mmb: no CUDA device available (the B200 path has no CPU fallback)");
+        if (d.device < 0 || d.device >= ndev) throw std::invalid_argument("mmb: bad device ordinal");
+        ck(cudaSetDevice(d.device), "cudaSetDevice");
+        ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+
+        Geom& g = g_;
+        g.nx = d.nx;
+        g.ny = d.ny;
+        g.nz = d.nz;
+        g.lx = d.nx == 1 ? 1 : pow2_at_least(2 * d.nx - 1);
+        g.ly = d.ny == 1 ? 1 : pow2_at_least(2 * d.ny - 1);
+        g.lz = d.nz == 1 ? 1 : pow2_at_least(2 * d.nz - 1);
+        g.log2lx = ilog2(g.lx);
+        g.log2ly = ilog2(g.ly);
+        g.log2lz = ilog2(g.lz);
+        if (g.log2lx > 12 || g.log2ly > 12 || g.log2lz > 12)
+            throw std::invalid_argument("mmb: grid axis too long (max 2048 cells per axis)");
+        g.xh = g.lx == 1 ? 1 : g.lx / 2 + 1;
+        g.xp = (g.xh + 15) / 16 * 16;
+        g.yh = g.ly == 1 ? 1 : g.ly / 2 + 1;
+        g.zh = g.lz == 1 ? 1 : g.lz / 2 + 1;
+        g.n = static_cast<long long>(d.nx) * d.ny * d.nz;
+        g.rows = static_cast<long long>(d.ny) * d.nz;
+
+        const size_t n = static_cast<size_t>(g.n);
+        m_[0].alloc(3 * n);
+        m_[1].alloc(3 * n);
+        hd_.alloc(3 * n);
+        heff_.alloc(3 * n);
+        S_.alloc(static_cast<size_t>(3) * g.nz * g.ly * g.xp);
+        kspec_.alloc(static_cast<size_t>(6) * g.zh * g.yh * g.xh);
+        twx_.alloc(g.lx);
+        twy_.alloc(g.ly);
+        twz_.alloc(g.lz);
+        partial_.alloc(3 * 1024);
+        red_.alloc(8);
+        ctl_.alloc(1);
+        ck(cudaMallocHost(&ctl_host_, sizeof(StepCtl)), "cudaMallocHost");
+
+        launch_twiddles<T>(twx_.p, g.lx, stream_);
+        launch_twiddles<T>(twy_.p, g.ly, stream_);
+        launch_twiddles<T>(twz_.p, g.lz, stream_);
+        prepare_fft_kernels<T>(g_);
+
+        // StepCtl: step 0, alpha from the material (llg.cpp:31-33).
+        StepCtl c{};
+        c.step = 0;
+        c.cur_step = 0;
+        c.alpha = d.alpha;
+        c.dt = d.dt;
+        c.ms = d.ms;
+        c.bad_key = ~0ull;
+        ck(cudaMemcpyAsync(ctl_.p, &c, sizeof(c), cudaMemcpyHostToDevice, stream_), "ctl upload");
+
+        // Tensor entries on device (K0), then the spectrum.
+        DevBuf<double> E;
+        E.alloc(6 * n);
+        launch_tensor_octant(E.p, g.nx, g.ny, g.nz, d.delta, stream_);
+        build_spectrum(E.p);
+
+        // init_uniform (proj/include/mmsim/vector_field.hpp:41-52)
+        const double norm = std::sqrt(d.init_dir[0] * d.init_dir[0] + d.init_dir[1] * d.init_dir[1] +
+                                      d.init_dir[2] * d.init_dir[2]);
+        if (!(norm > 0.0)) throw std::invalid_argument("init_uniform: direction vector must be nonzero");
+        std::vector<T> col(n);
+        for (int c3 = 0; c3 < 3; ++c3) {
+            std::fill(col.begin(), col.end(), static_cast<T>(d.ms * d.init_dir[c3] / norm));
+            ck(cudaMemcpyAsync(m_[0].p + c3 * n, col.data(), n * sizeof(T), cudaMemcpyHostToDevice,
+                               stream_), "M upload");
+            ck(cudaStreamSynchronize(stream_), "sync");
+        }
+        cur_ = 0;
+        exch_coeff_ = 2.0 * d.a_ex / (kMu0 * d.ms * d.ms * d.delta * d.delta); // material.hpp:27-29
+        aniso_coeff_ = d.hk / d.ms;                                           // local_fields.hpp:27
+        ck(cudaStreamSynchronize(stream_), "create sync");
+    }
+
+    ~Solver() override {
+        for (auto& ge : graph_)
+            if (ge) cudaGraphExecDestroy(ge);
+        if (ctl_host_) cudaFreeHost(ctl_host_);
+        if (stream_) cudaStreamDestroy(stream_);
+    }
+
+    int precision() const override { return sizeof(T) == 8 ? MMB_F64 : MMB_F32; }
+
+    void set_m(const void* x, const void* y, const void* z) override {
+        const size_t n = g_.n;
+        const void* src[3] = {x, y, z};
+        for (int c = 0; c < 3; ++c)
+            ck(cudaMemcpyAsync(m_[cur_].p + c * n, src[c], n * sizeof(T), cudaMemcpyHostToDevice, stream_),
+               "set_m");
+        ck(cudaStreamSynchronize(stream_), "set_m sync");
+    }
+
+    void get_m(void* x, void* y, void* z) override {
+        const size_t n = g_.n;
+        void* dst[3] = {x, y, z};
+        for (int c = 0; c < 3; ++c)
+            ck(cudaMemcpyAsync(dst[c], m_[cur_].p + c * n, n * sizeof(T), cudaMemcpyDeviceToHost, stream_),
+               "get_m");
+        sync_and_check();
+    }
+
+    void step(long long n) override {
+        for (long long i = 0; i < n; ++i) {
+            ensure_graph(cur_);
+            ck(cudaGraphLaunch(graph_[cur_], stream_), "cudaGraphLaunch");
+            cur_ ^= 1;
+            ++step_;
+        }
+    }
+
+    long long step_index() const override { return step_; }
+
+    void average(double* out) override {
+        // average_magnetization (vector_field.hpp:86-99) / average_unit (llg.cpp:126-131)
+        launch_sum3<T>(m_[cur_].p, g_.n, partial_.p, red_.p, stream_);
+        double s[3];
+        ck(cudaMemcpyAsync(s, red_.p, sizeof(s), cudaMemcpyDeviceToHost, stream_), "average");
+        sync_and_check();
+        const double inv = 1.0 / static_cast<double>(g_.n);
+        const double inv_ms = 1.0 / d_.ms;
+        for (int c = 0; c < 3; ++c) out[c] = (inv * s[c]) * inv_ms;
+    }
+
+    double energy() override {
+        // Simulation<T>::energy (llg.cpp:133-138): applied field at step_ (no alpha update),
+        // demag recomputed, total_energy (energy.cpp:39-64).
+        enqueue_demag(m_[cur_].p, hd_.p, 3);
+        const double ms = d_.ms;
+        const double ku = 0.5 * d_.hk * kMu0 * ms;
+        launch_energy<T>(m_[cur_].p, hd_.p, g_, ku / (ms * ms), ctl_.p, partial_.p, red_.p, stream_);
+        double e[2];
+        ck(cudaMemcpyAsync(e, red_.p, sizeof(e), cudaMemcpyDeviceToHost, stream_), "energy");
+        sync_and_check();
+        return e[0] * (d_.delta * d_.delta * d_.delta) + d_.a_ex * d_.delta / (ms * ms) * e[1];
+    }
+
+    double max_torque() override {
+        // llg.cpp:140-156: re-assemble H_eff (may apply the sticky alpha override).
+        enqueue_heff();
+        launch_torque_max<T>(m_[cur_].p, heff_.p, g_.n,
+                             reinterpret_cast<unsigned long long*>(red_.p + 4), stream_);
+        double sq;
+        ck(cudaMemcpyAsync(&sq, red_.p + 4, sizeof(sq), cudaMemcpyDeviceToHost, stream_), "torque");
+        sync_and_check();
+        return std::sqrt(sq) / (d_.ms * d_.ms);
+    }
+
+    double last_torque_sq() override {
+        fetch_ctl();
+        double v;
+        std::memcpy(&v, &ctl_host_->torque_sq_bits, sizeof(v));
+        return v;
+    }
+
+    long long run(long long steps, long long cadence, double stop_torque, mmb_record_fn fn,
+                  void* user) override {
+        // Simulation<T>::run (llg.cpp:110-124): record on absolute step_ % cadence == 0, stop
+        // when sqrt(last_torque_sq)/ms^2 < stop_torque.
+        const double ms2 = d_.ms * d_.ms;
+        long long done = 0;
+        const bool stop = stop_torque >= 0.0;
+        while (done < steps) {
+            // Batch graph replays up to the next record point when no per-step check is needed.
+            long long chunk = steps - done;
+            if (fn && cadence > 0) chunk = std::min(chunk, cadence - (step_ % cadence));
+            if (stop) chunk = 1;
+            step(chunk);
+            done += chunk;
+            if (fn && cadence > 0 && step_ % cadence == 0) {
+                double a[3];
+                average(a);
+                fn(user, step_, a[0], a[1], a[2]);
+            }
+            if (stop && std::sqrt(last_torque_sq()) / ms2 < stop_torque) break;
+        }
+        sync_and_check();
+        return done;
+    }
+
+    void synchronize() override { sync_and_check(); }
+
+    void effective_field(void* x, void* y, void* z) override {
+        enqueue_heff();
+        copy_out(heff_.p, x, y, z);
+    }
+
+    void demag_field(const void* mx, const void* my, const void* mz, void* hx, void* hy,
+                     void* hz) override {
+        const size_t n = g_.n;
+        const void* src[3] = {mx, my, mz};
+        for (int c = 0; c < 3; ++c)
+            ck(cudaMemcpyAsync(heff_.p + c * n, src[c], n * sizeof(T), cudaMemcpyHostToDevice, stream_),
+               "demag upload");
+        enqueue_demag(heff_.p, hd_.p, 0);
+        copy_out(hd_.p, hx, hy, hz);
+    }
+
+    void tensor_octant(double* out) override {
+        DevBuf<double> E;
+        E.alloc(6 * static_cast<size_t>(g_.n));
+        launch_tensor_octant(E.p, g_.nx, g_.ny, g_.nz, d_.delta, stream_);
+        ck(cudaMemcpyAsync(out, E.p, E.bytes(), cudaMemcpyDeviceToHost, stream_), "octant");
+        sync_and_check();
+    }
+
+    void upload_tensor_octant(const double* entries) override {
+        DevBuf<double> E;
+        E.alloc(6 * static_cast<size_t>(g_.n));
+        ck(cudaMemcpyAsync(E.p, entries, E.bytes(), cudaMemcpyHostToDevice, stream_), "octant upload");
+        build_spectrum(E.p);
+        sync_and_check();
+    }
+
+    float time_steps(long long n) override {
+        ensure_graph(0);
+        ensure_graph(1);
+        cudaEvent_t a, b;
+        ck(cudaEventCreate(&a), "event");
+        ck(cudaEventCreate(&b), "event");
+        ck(cudaEventRecord(a, stream_), "record");
+        step(n);
+        ck(cudaEventRecord(b, stream_), "record");
+        ck(cudaEventSynchronize(b), "event sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        check_numerical();
+        return ms;
+    }
+
+    int profile_step(long long n, float* out, int maxk, std::string& names) override {
+        // Eager launches with an event between kernels; per-kernel mean over n steps.
+        const std::vector<std::string> kn = kernel_names();
+        const int nk = static_cast<int>(kn.size());
+        std::vector<cudaEvent_t> ev(nk + 1);
+        for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+        std::vector<double> acc(nk, 0.0);
+        for (long long s = 0; s < n; ++s) {
+            ck(cudaEventRecord(ev[0], stream_), "record");
+            enqueue_step_eager(cur_, ev.data());
+            ck(cudaEventSynchronize(ev[nk]), "sync");
+            for (int k = 0; k < nk; ++k) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+                acc[k] += ms;
+            }
+            cur_ ^= 1;
+            ++step_;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        names.clear();
+        for (int k = 0; k < nk; ++k) {
+            if (k < maxk) out[k] = static_cast<float>(acc[k] / std::max<long long>(1, n));
+            names += kn[k];
+            if (k + 1 < nk) names += ";";
+        }
+        check_numerical();
+        return nk;
+    }
+
+    int launches_per_step() const override { return static_cast<int>(kernel_names().size()); }
+
+    size_t device_bytes() const override {
+        return m_[0].bytes() + m_[1].bytes() + hd_.bytes() + heff_.bytes() + S_.bytes() +
+               kspec_.bytes() + twx_.bytes() + twy_.bytes() + twz_.bytes() + partial_.bytes() +
+               red_.bytes() + ctl_.bytes();
+    }
+
+private:
+    void set_schedule(const mmb_stage* stages, int n) {
+        // FieldSchedule ctor validation (proj/src/schedule.cpp:8-17)
+        if (n < 0 || (n > 0 && !stages)) throw std::invalid_argument("mmb: bad stage list");
+        if (n > kMaxStages) throw std::invalid_argument("mmb: too many schedule stages (max 16)");
+        std::vector<mmb_stage> s(stages, stages + n);
+        std::stable_sort(s.begin(), s.end(),
+                         [](const mmb_stage& a, const mmb_stage& b) { return a.start < b.start; });
+        for (size_t i = 0; i < s.size(); ++i) {
+            if (s[i].end <= s[i].start)
+                throw std::invalid_argument("FieldSchedule: stage range must be nonempty");
+            if (i > 0 && s[i].start < s[i - 1].end)
+                throw std::invalid_argument("FieldSchedule: stage ranges must be disjoint");
+        }
+        std::memset(&st_, 0, sizeof(st_));
+        st_.n = n;
+        for (int i = 0; i < n; ++i) {
+            st_.start[i] = s[i].start;
+            st_.end[i] = s[i].end;
+            st_.ramp[i] = s[i].ramp;
+            st_.has_alpha[i] = s[i].has_alpha;
+            st_.alpha[i] = s[i].alpha_override;
+            for (int c = 0; c < 3; ++c) {
+                st_.field[i][c] = s[i].field[c];
+                st_.field_end[i][c] = s[i].field_end[c];
+            }
+        }
+    }
+
+    void build_spectrum(const double* E) {
+        const Geom& g = g_;
+        DevBuf<double2> csx, csy, csz;
+        csx.alloc(g.lx);
+        csy.alloc(g.ly);
+        csz.alloc(g.lz);
+        launch_cs_table(csx.p, g.lx, stream_);
+        launch_cs_table(csy.p, g.ly, stream_);
+        launch_cs_table(csz.p, g.lz, stream_);
+        const long long c0 = g.n;
+        const long long c1 = static_cast<long long>(g.xh) * g.ny * g.nz;
+        const long long c2 = static_cast<long long>(g.xh) * g.yh * g.nz;
+        const long long c3 = static_cast<long long>(g.xh) * g.yh * g.zh;
+        DevBuf<double> a1, a2, a3;
+        a1.alloc(6 * c1);
+        launch_axis_transform(E, a1.p, g.nx, g.ny, g.nz, 0, g.lx, csx.p, 0x06, c0, c1, stream_);
+        a2.alloc(6 * c2);
+        launch_axis_transform(a1.p, a2.p, g.xh, g.ny, g.nz, 1, g.ly, csy.p, 0x12, c1, c2, stream_);
+        a3.alloc(6 * c3);
+        launch_axis_transform(a2.p, a3.p, g.xh, g.yh, g.nz, 2, g.lz, csz.p, 0x14, c2, c3, stream_);
+        const double scale = 1.0 / (static_cast<double>(g.lx) * g.ly * g.lz);
+        launch_tensor_finalize<T>(a3.p, kspec_.p, c3, scale, stream_);
+        ck(cudaStreamSynchronize(stream_), "spectrum sync");
+    }
+
+    std::vector<std::string> kernel_names() const {
+        if (g_.nz == 1) return {"x_fwd", "y_mac", "x_inv", "llg"};
+        return {"x_fwd", "y_fwd", "z_mac", "y_inv", "x_inv", "llg"};
+    }
+
+    // Demag of m into h; prologue: 0 none, 1 stepping, 2 assembly, 3 applied field only.
+    void enqueue_demag(const T* m, T* h, int prologue, cudaEvent_t* ev = nullptr) {
+        int k = 1;
+        auto mark = [&]() {
+            if (ev) ck(cudaEventRecord(ev[k++], stream_), "record");
+        };
+        launch_x_fwd<T>(m, S_.p, g_, twx_.p, ctl_.p, st_, prologue, stream_);
+        mark();
+        if (g_.nz == 1) {
+            launch_y_mac<T>(S_.p, g_, twy_.p, kspec_.p, stream_);
+            mark();
+        } else {
+            launch_y<T>(0, S_.p, g_, twy_.p, stream_);
+            mark();
+            launch_z_mac<T>(S_.p, g_, twz_.p, kspec_.p, stream_);
+            mark();
+            launch_y<T>(1, S_.p, g_, twy_.p, stream_);
+            mark();
+        }
+        launch_x_inv<T>(S_.p, h, g_, twx_.p, stream_);
+        mark();
+    }
+
+    void enqueue_step_eager(int cur, cudaEvent_t* ev = nullptr) {
+        enqueue_demag(m_[cur].p, hd_.p, 1, ev);
+        launch_llg<T>(0, m_[cur].p, hd_.p, m_[cur ^ 1].p, g_, exch_coeff_, aniso_coeff_, ctl_.p, stream_);
+        if (ev) ck(cudaEventRecord(ev[kernel_names().size()], stream_), "record");
+    }
+
+    void enqueue_heff() {
+        enqueue_demag(m_[cur_].p, hd_.p, 2);
+        launch_llg<T>(1, m_[cur_].p, hd_.p, heff_.p, g_, exch_coeff_, aniso_coeff_, ctl_.p, stream_);
+    }
+
+    void ensure_graph(int cur) {
+        if (graph_[cur]) return;
+        cudaGraph_t gr;
+        ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+        enqueue_step_eager(cur);
+        ck(cudaStreamEndCapture(stream_, &gr), "end capture");
+        ck(cudaGraphInstantiate(&graph_[cur], gr, 0), "graph instantiate");
+        cudaGraphDestroy(gr);
+    }
+
+    void copy_out(const T* src, void* x, void* y, void* z) {
+        const size_t n = g_.n;
+        void* dst[3] = {x, y, z};
+        for (int c = 0; c < 3; ++c)
+            ck(cudaMemcpyAsync(dst[c], src + c * n, n * sizeof(T), cudaMemcpyDeviceToHost, stream_), "copy out");
+        sync_and_check();
+    }
+
+    void fetch_ctl() {
+        ck(cudaMemcpyAsync(ctl_host_, ctl_.p, sizeof(StepCtl), cudaMemcpyDeviceToHost, stream_), "ctl");
+        ck(cudaStreamSynchronize(stream_), "ctl sync");
+    }
+
+    void check_numerical() {
+        fetch_ctl();
+        const unsigned long long key = ctl_host_->bad_key;
+        if (key != ~0ull) {
+            const long long cell = static_cast<long long>(key & ((1ull << 36) - 1));
+            const long long st = static_cast<long long>(key >> 36);
+            // reset so the handle can report later failures
+            const unsigned long long none = ~0ull;
+            ck(cudaMemcpyAsync(&ctl_.p->bad_key, &none, sizeof(none), cudaMemcpyHostToDevice, stream_), "reset");
+            ck(cudaStreamSynchronize(stream_), "reset sync");
+            throw numerical_error("renormalize: zero-magnitude magnetization at cell " +
+                                  std::to_string(cell) + " at step " + std::to_string(st));
+        }
+    }
+
+    void sync_and_check() {
+        ck(cudaStreamSynchronize(stream_), "sync");
+        check_numerical();
+    }
+
+    mmb_desc d_;
+    Geom g_{};
+    StageTable st_{};
+    cudaStream_t stream_ = nullptr;
+    DevBuf<T> m_[2], hd_, heff_;
+    DevBuf<cx<T>> S_, twx_, twy_, twz_;
+    DevBuf<T> kspec_;
+    DevBuf<double> partial_, red_;
+    DevBuf<StepCtl> ctl_;
+    StepCtl* ctl_host_ = nullptr;
+    cudaGraphExec_t graph_[2] = {nullptr, nullptr};
+    int cur_ = 0;
+    long long step_ = 0;
+    double exch_coeff_ = 0.0, aniso_coeff_ = 0.0;
+};
+
+} // namespace mmb
+
+// ------------------------------------------------------------------------------ C-ABI
+struct mmb_ctx {
+    std::unique_ptr<mmb::SolverBase> s;
+};
+
+namespace {
+
+thread_local std::string t_last_error;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        return fn();
+    } catch (const mmb::numerical_error& e) {
+        t_last_error = e.what();
+        return MMB_ERROR_NUMERICAL;
+    } catch (const std::invalid_argument& e) {
+        t_last_error = e.what();
+        return MMB_ERROR_ARGUMENT;
+    } catch (const std::bad_alloc&) {
+        t_last_error = "out of memory";
+        return MMB_ERROR_NOMEM;
+    } catch (const mmb::cuda_error& e) {
+        t_last_error = e.what();
+        return MMB_ERROR_CUDA;
+    } catch (const std::exception& e) {
+        t_last_error = e.what();
+        return MMB_ERROR_INTERNAL;
+    } catch (...) {
+        t_last_error = "unknown error";
+        return MMB_ERROR_INTERNAL;
+    }
+}
+
+int bad(const char* what) {
+    t_last_error = std::string(what) + ": NULL or invalid argument";
+    return MMB_ERROR_ARGUMENT;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* mmb_status_string(int status) {
+    switch (status) {
+        case MMB_OK: return "ok";
+        case MMB_ERROR_ARGUMENT: return "invalid argument";
+        case MMB_ERROR_CONFIG: return "configuration error";
+        case MMB_ERROR_NUMERICAL: return "numerical failure";
+        case MMB_ERROR_IO: return "i/o error";
+        case MMB_ERROR_NOMEM: return "out of memory";
+        case MMB_ERROR_VALIDATION: return "validation failure";
+        case MMB_ERROR_INTERNAL: return "internal error";
+        case MMB_ERROR_CUDA: return "cuda error";
+        default: return "unknown status";
+    }
+}
+
+const char* mmb_last_error(void) { return t_last_error.c_str(); }
+const char* mmb_version(void) { return "0.1.0-b200"; }
+
+int mmb_create(const mmb_desc* desc, const mmb_stage* stages, int nstages, mmb_ctx** out) {
+    if (!desc || !out) return bad("mmb_create");
+    *out = nullptr;
+    return guarded([&] {
+        auto h = std::make_unique<mmb_ctx>();
+        if (desc->precision == MMB_F64) h->s = std::make_unique<mmb::Solver<double>>(*desc, stages, nstages);
+        else if (desc->precision == MMB_F32) h->s = std::make_unique<mmb::Solver<float>>(*desc, stages, nstages);
+        else throw std::invalid_argument("unknown precision (expected MMB_F32 or MMB_F64)");
+        *out = h.release();
+        return MMB_OK;
+    });
+}
+
+void mmb_free(mmb_ctx* ctx) { delete ctx; }
+
+int mmb_set_m(mmb_ctx* ctx, const void* x, const void* y, const void* z) {
+    if (!ctx || !x || !y || !z) return bad("mmb_set_m");
+    return guarded([&] { ctx->s->set_m(x, y, z); return MMB_OK; });
+}
+
+int mmb_get_m(mmb_ctx* ctx, void* x, void* y, void* z) {
+    if (!ctx || !x || !y || !z) return bad("mmb_get_m");
+    return guarded([&] { ctx->s->get_m(x, y, z); return MMB_OK; });
+}
+
+int mmb_step(mmb_ctx* ctx, long long n) {
+    if (!ctx || n < 0) {
+        t_last_error = "mmb_step: bad handle or negative count";
+        return MMB_ERROR_ARGUMENT;
+    }
+    return guarded([&] { ctx->s->step(n); return MMB_OK; });
+}
+
+int mmb_step_index(const mmb_ctx* ctx, long long* out) {
+    if (!ctx || !out) return bad("mmb_step_index");
+    *out = ctx->s->step_index();
+    return MMB_OK;
+}
+
+int mmb_average(mmb_ctx* ctx, double out[3]) {
+    if (!ctx || !out) return bad("mmb_average");
+    return guarded([&] { ctx->s->average(out); return MMB_OK; });
+}
+
+int mmb_energy(mmb_ctx* ctx, double* out) {
+    if (!ctx || !out) return bad("mmb_energy");
+    return guarded([&] { *out = ctx->s->energy(); return MMB_OK; });
+}
+
+int mmb_max_torque(mmb_ctx* ctx, double* out) {
+    if (!ctx || !out) return bad("mmb_max_torque");
+    return guarded([&] { *out = ctx->s->max_torque(); return MMB_OK; });
+}
+
+int mmb_last_torque_sq(mmb_ctx* ctx, double* out) {
+    if (!ctx || !out) return bad("mmb_last_torque_sq");
+    return guarded([&] { *out = ctx->s->last_torque_sq(); return MMB_OK; });
+}
+
+int mmb_run(mmb_ctx* ctx, long long steps, long long cadence, double stop_torque,
+            mmb_record_fn record, void* user, long long* steps_done) {
+    if (!ctx || steps < 0) return bad("mmb_run");
+    return guarded([&] {
+        const long long d = ctx->s->run(steps, cadence, stop_torque, record, user);
+        if (steps_done) *steps_done = d;
+        return MMB_OK;
+    });
+}
+
+int mmb_synchronize(mmb_ctx* ctx) {
+    if (!ctx) return bad("mmb_synchronize");
+    return guarded([&] { ctx->s->synchronize(); return MMB_OK; });
+}
+
+int mmb_effective_field(mmb_ctx* ctx, void* hx, void* hy, void* hz) {
+    if (!ctx || !hx || !hy || !hz) return bad("mmb_effective_field");
+    return guarded([&] { ctx->s->effective_field(hx, hy, hz); return MMB_OK; });
+}
+
+int mmb_demag_field(mmb_ctx* ctx, const void* mx, const void* my, const void* mz, void* hx,
+                    void* hy, void* hz) {
+    if (!ctx || !mx || !my || !mz || !hx || !hy || !hz) return bad("mmb_demag_field");
+    return guarded([&] { ctx->s->demag_field(mx, my, mz, hx, hy, hz); return MMB_OK; });
+}
+
+int mmb_tensor_octant(mmb_ctx* ctx, double* out) {
+    if (!ctx || !out) return bad("mmb_tensor_octant");
+    return guarded([&] { ctx->s->tensor_octant(out); return MMB_OK; });
+}
+
+int mmb_upload_tensor_octant(mmb_ctx* ctx, const double* entries) {
+    if (!ctx || !entries) return bad("mmb_upload_tensor_octant");
+    return guarded([&] { ctx->s->upload_tensor_octant(entries); return MMB_OK; });
+}
+
+int mmb_time_steps(mmb_ctx* ctx, long long n, float* ms) {
+    if (!ctx || !ms || n < 0) return bad("mmb_time_steps");
+    return guarded([&] { *ms = ctx->s->time_steps(n); return MMB_OK; });
+}
+
+int mmb_profile_step(mmb_ctx* ctx, long long n, float* kernel_ms, int max_kernels, int* count,
+                     char* names_buf, size_t names_len) {
+    if (!ctx || !kernel_ms || !count || n < 1) return bad("mmb_profile_step");
+    return guarded([&] {
+        std::string names;
+        *count = ctx->s->profile_step(n, kernel_ms, max_kernels, names);
+        if (names_buf && names_len) {
+            const size_t k = std::min(names.size(), names_len - 1);
+            std::memcpy(names_buf, names.data(), k);
+            names_buf[k] = 0;
+        }
+        return MMB_OK;
+    });
+}
+
+int mmb_launches_per_step(mmb_ctx* ctx, int* out) {
+    if (!ctx || !out) return bad("mmb_launches_per_step");
+    *out = ctx->s->launches_per_step();
+    return MMB_OK;
+}
+
+int mmb_device_bytes(mmb_ctx* ctx, size_t* out) {
+    if (!ctx || !out) return bad("mmb_device_bytes");
+    *out = ctx->s->device_bytes();
+    return MMB_OK;
+}
+
+} // extern "C"

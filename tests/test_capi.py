@@ -1,0 +1,77 @@
+"""CPU tests of the product boundary: libmmb.so builds, loads, exports every symbol
+include/mmb.h declares, and fails loudly (no CPU fallback) when no GPU is present; host-side
+spec types mirror the reference's validation."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_1501_07293_b200 import _lib
+from paper_1501_07293_b200.problems import (FieldSchedule, Grid, MaterialParams, ScheduleStage,
+                                            standard_problem_3_benchmark, standard_problem_4)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "mmb.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mmb_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert _declared() == sorted(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.load()
+    for name in _declared():
+        assert hasattr(L, name), name
+    assert L.mmb_version().decode().startswith("0.1")
+    assert L.mmb_status_string(3).decode() == "numerical failure"
+
+
+def test_sm100a_code_in_library():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_argument_errors_without_device():
+    L = _lib.load()
+    assert L.mmb_create(None, None, 0, None) == _lib.MMB_ERROR_ARGUMENT
+    assert L.mmb_step(None, 1) == _lib.MMB_ERROR_ARGUMENT
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    L = _lib.load()
+    desc = _lib.MmbDesc(4, 4, 1, 1.0, 1e7, 800.0, 0.0, 0.5, 1e-5, (C.c_double * 3)(1, 0, 0),
+                        _lib.MMB_F64, 0)
+    h = C.c_void_p()
+    rc = L.mmb_create(C.byref(desc), None, 0, C.byref(h))
+    assert rc == _lib.MMB_ERROR_CUDA
+    assert "no CUDA device" in L.mmb_last_error().decode()
+
+
+def test_host_spec_validation():
+    with pytest.raises(ValueError):
+        Grid(0, 1, 1, 1.0)
+    with pytest.raises(ValueError):
+        MaterialParams(ms=0.0).validate()
+    a, b = ScheduleStage(0, 10), ScheduleStage(5, 15)
+    with pytest.raises(ValueError):
+        FieldSchedule([a, b])
+    with pytest.raises(ValueError):
+        FieldSchedule([ScheduleStage(10, 10)])
+    assert FieldSchedule().at(123) == ((0.0, 0.0, 0.0), None)
+    sp4 = standard_problem_4()
+    assert sp4.grid.nx == 166 and sp4.schedule.at(60000)[1] == 0.02
+    ramp = sp4.schedule.stages()[1]
+    assert ramp.value_at(ramp.end)[0] == 0.0
+    assert standard_problem_3_benchmark(8).material.hk == 100.0
+    assert abs(MaterialParams(1.3e7, 800.0).exchange_coefficient(1.0) - 32.33) <= 0.01

@@ -1,0 +1,268 @@
+"""GPU parity: the B200 path (libmmb.so through the Python mirror / C-ABI) against the reference
+solver (oracle/_ref, compiled from the reference sources) and the committed golden vectors.
+
+Tolerances are the north star's, with the reference's own metric (max |a-b| / max |b|,
+proj/src/validate.cpp:41-53): H_eff <= 1e-12 (f64) / 1e-5 (f32); <m>(t) <= 1e-6 (f64) /
+1e-3 (f32). Tensor entries: 1e-13 absolute (proj/tests/test_demag_tensor.cpp:86-91).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import mmsim_oracle as O
+from paper_1501_07293_b200 import RunOptions
+from paper_1501_07293_b200._lib import NumericalError
+
+from .helpers import b200, octant_from_shifted, ref_problem, rel, sp4, spec
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden")
+TOL_H = {"f64": 1e-12, "f32": 1e-5}
+
+GRIDS = [
+    (1, 1, 1, 2.0), (2, 2, 2, 1.0), (3, 3, 3, 2.0), (4, 4, 2, 1.0), (5, 3, 2, 3.0), (7, 1, 1, 1.0),
+    (1, 6, 2, 1.0), (8, 8, 4, 1.0), (6, 5, 3, 1.0), (16, 12, 3, 2.5), (33, 17, 1, 3.0),
+    (128, 32, 1, 3.90625), (166, 42, 1, 3.0), (40, 24, 9, 2.0), (64, 64, 1, 1.0), (1, 1, 17, 1.0),
+]
+
+
+@pytest.mark.parametrize("grid", GRIDS)
+def test_tensor_entries_match_reference(refsolver, grid):
+    nx, ny, nz, delta = grid
+    sim = b200(spec(nx, ny, nz, delta))
+    got = sim.tensor_octant()
+    want = octant_from_shifted(refsolver.build_tensor(nx, ny, nz, delta), nx, ny, nz)
+    assert np.max(np.abs(got - want)) <= 1e-13
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("grid", GRIDS)
+def test_demag_field_matches_reference(refsolver, grid, prec):
+    nx, ny, nz, delta = grid
+    dt = np.float64 if prec == "f64" else np.float32
+    sp = spec(nx, ny, nz, delta)
+    sim = b200(sp, prec)
+    m = refsolver.random_unit_field(nx, ny, nz, 800.0, 20240 + nx, dt)
+    want = refsolver.heff(ref_problem(refsolver, sp), m, parts=1)
+    assert rel(sim.demag_field(m), want) <= TOL_H[prec]
+    # with the reference's own fp64 tensor uploaded (isolates the per-step kernels)
+    sim.upload_tensor_octant(octant_from_shifted(refsolver.build_tensor(nx, ny, nz, delta), nx, ny, nz))
+    assert rel(sim.demag_field(m), want) <= TOL_H[prec]
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_demag_fft_vs_direct_sum(refsolver, prec):
+    # proj/tests/test_demag_field.cpp:150-172 criterion on the B200 path
+    tol = 1e-10 if prec == "f64" else 1e-4
+    for nx, ny, nz, delta in [(2, 2, 2, 1.0), (3, 3, 3, 2.0), (4, 4, 2, 1.0), (5, 3, 2, 3.0),
+                              (7, 1, 1, 1.0), (1, 6, 2, 1.0), (8, 8, 4, 1.0)]:
+        sp = spec(nx, ny, nz, delta)
+        m = refsolver.random_unit_field(nx, ny, nz, 800.0, 1000 + nx, np.float64)
+        direct = refsolver.demag_direct(ref_problem(refsolver, sp), m)
+        got = b200(sp, prec).demag_field(m.astype(np.float64 if prec == "f64" else np.float32))
+        assert rel(got, direct) <= tol
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_effective_field_matches_golden(prec):
+    d = np.load(os.path.join(GOLD, "fields_small.npz"))
+    for idx, row in enumerate(d["cases"]):
+        nx, ny, nz = int(row[0]), int(row[1]), int(row[2])
+        delta, a_ex, ms, hk, alpha = (float(v) for v in row[3:8])
+        applied = tuple(float(v) for v in row[8:11])
+        sp = spec(nx, ny, nz, delta, a_ex, ms, hk, alpha, 5e-6, [(0, 1_000_000, applied)])
+        sim = b200(sp, prec)
+        sim.set_magnetization(d[f"c{idx}_{prec}_m0"])
+        assert rel(sim.effective_field(), d[f"c{idx}_{prec}_heff"]) <= TOL_H[prec], idx
+        sim.step(10)
+        tol = 1e-11 if prec == "f64" else 2e-5
+        assert rel(sim.magnetization(), d[f"c{idx}_{prec}_m10"]) <= tol, idx
+        assert np.max(np.abs(np.array(sim.average_unit()) - d[f"c{idx}_{prec}_avg10"])) <= tol
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("grid", [(16, 12, 3, 2.5), (40, 24, 9, 2.0), (166, 42, 1, 3.0), (64, 64, 1, 1.0)])
+def test_steps_match_reference(refsolver, grid, prec):
+    nx, ny, nz, delta = grid
+    dt = np.float64 if prec == "f64" else np.float32
+    sp = spec(nx, ny, nz, delta, 1.3e7, 800.0, 30.0, 0.5, 5e-6,
+              [(0, 20, (10.0, -20.0, 5.0)), (20, 40, (0.0, 50.0, 0.0), True, (40.0, 0.0, 0.0), 0.1)])
+    m0 = refsolver.random_unit_field(nx, ny, nz, 800.0, 77 + nx, dt)
+    sim = b200(sp, prec)
+    sim.set_magnetization(m0)
+    r = refsolver.RefSimulation(ref_problem(refsolver, sp), prec)
+    r.set_m(m0)
+    for chunk in (1, 9, 15, 15):  # crosses the ramp stage and the sticky alpha override
+        sim.step(chunk)
+        r.step(chunk)
+        assert sim.step_index() == r.step_index()
+        tol = 1e-10 if prec == "f64" else 1e-4
+        assert rel(sim.magnetization(), r.get_m()) <= tol
+        assert np.max(np.abs(np.array(sim.average_unit()) - np.array(r.average_unit()))) <= tol
+        # H_eff assembled at the same (post-override) state
+        assert rel(sim.effective_field(), refsolver.heff(ref_problem(refsolver, sp), r.get_m(),
+                                                         sp.schedule.at(r.step_index())[0])) <= 100 * TOL_H[prec]
+    assert abs(sim.max_torque() - r.max_torque()) <= (1e-9 if prec == "f64" else 1e-4) * r.max_torque()
+    e_b, e_r = sim.energy(), r.energy()
+    assert abs(e_b - e_r) <= (1e-9 if prec == "f64" else 1e-4) * abs(e_r)
+
+
+# ---------------------------------------------------------------- reference test ports
+def single_cell(ms, alpha, dt, applied):
+    return spec(1, 1, 1, 1.0, 0.0, ms, 0.0, alpha, dt, [(0, 1_000_000, applied)])
+
+
+def test_fixed_point():
+    # proj/tests/test_llg.cpp:61-74
+    ms = 800.0
+    sim = b200(single_cell(ms, 0.5, 1e-3, (50.0, 0.0, 0.0)))
+    mx0 = sim.magnetization()[0].ravel()[0]
+    sim.step(10)
+    m = sim.magnetization().ravel()
+    assert m[0] == mx0
+    assert abs(m[1]) <= 1e-12 * ms and abs(m[2]) <= 1e-12 * ms
+    assert sim.step_index() == 10
+
+
+def test_hand_euler_step():
+    # proj/tests/test_llg.cpp:76-95
+    ms, h, dt, alpha = 800.0, 40.0, 2e-5, 0.5
+    sim = b200(single_cell(ms, alpha, dt, (ms / 3.0, 0.0, h)))
+    sim.step()
+    p1 = -0.221 * dt / (1 + alpha * alpha)
+    p2 = p1 * alpha / ms
+    vy, vz = p1 * (-ms * h), p2 * (-ms * ms * h)
+    norm = math.sqrt(ms * ms + vy * vy + vz * vz)
+    np.testing.assert_allclose(sim.magnetization().ravel(), [ms * ms / norm, ms * vy / norm, ms * vz / norm],
+                               rtol=1e-12)
+
+
+def test_damping_rotates_toward_field():
+    sim = b200(single_cell(800.0, 0.5, 2e-5, (800.0 / 3.0, 25.0, 0.0)))
+    sim.step()
+    assert sim.magnetization()[1].ravel()[0] > 0.0
+
+
+def tiny_relaxation():
+    return spec(4, 4, 2, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5)
+
+
+def test_norms_and_records():
+    sim = b200(tiny_relaxation())
+    sim.run(RunOptions(steps=50))
+    m = sim.magnetization()
+    mag = np.sqrt((m ** 2).sum(axis=0))
+    assert np.max(np.abs(mag - 1000.0)) <= 1e-9 * 1000.0
+    recs = []
+    sim2 = b200(tiny_relaxation())
+    assert sim2.run(RunOptions(steps=0, cadence=10, sink=recs.append)) == 0
+    assert recs == [] and sim2.step_index() == 0
+    assert abs(sim2.average_unit()[0] - 1.0) <= 1e-12
+    sim2.run(RunOptions(steps=100, cadence=10, sink=recs.append))
+    assert len(recs) == 10 and recs[0].step == 10 and recs[-1].step == 100
+
+
+def test_identical_runs_identical_trajectories():
+    def once():
+        recs = []
+        s = b200(tiny_relaxation())
+        s.run(RunOptions(steps=100, cadence=10, sink=recs.append))
+        return [(r.step, r.mx, r.my, r.mz) for r in recs]
+    assert once() == once()
+
+
+def test_torque_stop_and_energy():
+    sp = single_cell(800.0, 0.5, 1e-3, (50.0, 0.0, 0.0))
+    sim = b200(sp)
+    assert sim.run(RunOptions(steps=1000, stop_torque=1e-4)) < 1000
+    s = b200(tiny_relaxation())
+    e0 = s.energy()
+    s.run(RunOptions(steps=100))
+    assert s.energy() < e0
+
+
+def test_degenerate_cell_is_numerical_error():
+    sp = spec(2, 1, 1, 1.0, 0.0, 800.0, 0.0, 0.5, 1e-5)
+    sim = b200(sp)
+    m = sim.magnetization()
+    m[:, 0, 0, 1] = 0.0
+    sim.set_magnetization(m)
+    sim.step(3)
+    with pytest.raises(NumericalError, match=r"zero-magnitude magnetization at cell 1 at step 0"):
+        sim.average_unit()
+
+
+def test_argument_errors():
+    with pytest.raises(ValueError):
+        b200(spec(4, 4, 1, 1.0, ms=-1.0))
+    with pytest.raises(ValueError):
+        b200(spec(4, 4, 1, 1.0, stages=[(0, 10), (5, 15)]))
+
+
+# ---------------------------------------------------------------- SP#4 trajectories
+def _load_traj(name):
+    p = os.path.join(GOLD, f"traj_{name}.tsv")
+    if not os.path.exists(p):
+        pytest.skip(f"golden trajectory {name} not generated")
+    return np.loadtxt(p, comments="#")
+
+
+def _crossing(rows, reversal=50000, dt=5e-6):
+    for i in range(1, len(rows)):
+        if rows[i - 1, 0] <= reversal:
+            continue
+        a, b = rows[i - 1, 1], rows[i, 1]
+        if a > 0.0 and b <= 0.0:
+            frac = a / (a - b)
+            return (rows[i - 1, 0] + frac * (rows[i, 0] - rows[i - 1, 0])) * dt
+    return None
+
+
+@pytest.mark.parametrize("name,grid,prec", [
+    ("sp4_166_f64", (166, 42, 3.0), "f64"), ("sp4_128_f64", (128, 32, 3.90625), "f64"),
+    ("sp4_166_f32", (166, 42, 3.0), "f32"), ("sp4_128_f32", (128, 32, 3.90625), "f32"),
+])
+def test_sp4_trajectory_matches_reference(name, grid, prec):
+    want = _load_traj(name)
+    sim = b200(sp4(*grid), prec)
+    recs = []
+    sim.run(RunOptions(steps=150000, cadence=1000, sink=recs.append))
+    got = np.array([[r.step, r.mx, r.my, r.mz] for r in recs])
+    assert got.shape == want.shape
+    assert np.array_equal(got[:, 0], want[:, 0])
+    tol = 1e-6 if prec == "f64" else 1e-3
+    assert np.max(np.abs(got[:, 1:] - want[:, 1:])) <= tol
+    # physics anchor (proj/tests/acceptance.cpp:274-281): crossing 0.08-0.20 ns after reversal
+    t = _crossing(got)
+    assert t is not None and 0.08 <= t - 50000 * 5e-6 <= 0.20
+    if name == "sp4_166_f64":
+        fixture = np.loadtxt(os.path.join(GOLD, "sp4_field1_reference.tsv"))
+        tf = _crossing(fixture)
+        assert abs(t - tf) <= 0.05 * tf
+        post = got[:, 0] > 50000
+        assert np.max(np.abs(got[post, 2] - fixture[post, 2])) <= 0.1
+
+
+# ---------------------------------------------------------------- full-size properties
+def test_512x512x8_f32_properties():
+    sp = spec(512, 512, 8, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5)
+    sim = b200(sp, "f32")
+    rng = np.random.default_rng(5)
+    m1 = rng.uniform(-1, 1, (3, 8, 512, 512)).astype(np.float32)
+    m2 = rng.uniform(-1, 1, (3, 8, 512, 512)).astype(np.float32)
+    h1, h2 = sim.demag_field(m1), sim.demag_field(m2)
+    hc = sim.demag_field((2.0 * m1 - 0.75 * m2).astype(np.float32))
+    assert rel(hc, 2.0 * h1.astype(np.float64) - 0.75 * h2) <= 1e-5  # linearity
+    # uniform M: cube-like slab field bounded by ms, and |M| = ms after steps
+    sim.set_magnetization(1000.0 * m1 / np.sqrt((m1.astype(np.float64) ** 2).sum(0)))
+    sim.step(5)
+    m = sim.magnetization().astype(np.float64)
+    assert np.max(np.abs(np.sqrt((m ** 2).sum(0)) - 1000.0)) <= 1e-3
+    # H_demag at full size vs the NumPy restatement in fp64
+    g = O.Grid(512, 512, 8, 1.0)
+    want = O.demag_field_fft(m1.astype(np.float64), g)
+    assert rel(sim.demag_field(m1), want) <= 1e-5
