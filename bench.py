@@ -55,13 +55,13 @@ def algorithmic_bytes(nx, ny, nz, w):
     padded = 3 * xh * ly * nz * 2 * w        # after the y-forward
     tensor = 6 * xh * yh * zh * w
     k = {"x_fwd": 3 * n * w + half, "x_inv": half + 3 * n * w, "llg": 9 * n * w}
-    if nz == 1:
-        k["y_mac"] = 2 * half + tensor
-    else:
-        k["y_fwd"] = half + padded
-        k["z_mac"] = 2 * padded + tensor
-        k["y_inv"] = padded + half
-    return sum(k.values()), k
+    canonical = sum(k.values()) + (2 * half + tensor if nz == 1 else 2 * half + 4 * padded + tensor)
+    # per-kernel algorithmic bytes of the kernels each path actually launches
+    k["y_mac"] = k["yz"] = 2 * half + tensor          # fused: padded spectrum stays on chip
+    k["y_fwd"] = half + padded
+    k["z_mac"] = 2 * padded + tensor
+    k["y_inv"] = padded + half
+    return canonical, k
 
 
 def load_peaks():

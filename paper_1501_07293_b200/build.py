@@ -30,6 +30,8 @@ COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relax
 UNITS = [
     ("fft_f32.o", "fft_kernels.cu", ["-DMMB_ONLY_F32"]),
     ("fft_f64.o", "fft_kernels.cu", ["-DMMB_ONLY_F64"]),
+    ("fast_f32.o", "fast_kernels.cu", ["-DMMB_ONLY_F32"]),
+    ("fast_f64.o", "fast_kernels.cu", ["-DMMB_ONLY_F64"]),
     ("llg.o", "llg_kernels.cu", ["--fmad=false"]),
     ("tensor.o", "tensor_kernels.cu", ["--fmad=false"]),
     ("solver.o", "solver.cu", []),

@@ -1,0 +1,502 @@
+// fast_kernels.cu — the fast demag path (sm_100a): three kernels per demag evaluation.
+//
+//   KX  (k_xf) : x-r2c of 2P consecutive rows of one (component, z) plane: two real rows
+//                packed per complex four-step FFT, pruned to the nx live cells, separated
+//                in shared memory and written kx-major: S[kx][c][z][y] (y fastest), so every
+//                kx owns one contiguous block of 3*nz*Ly complex values.
+//   KYZ (k_yz) : per kx block, entirely in shared memory: y-forward four-step FFT of the
+//                3*nz live rows (ny live inputs, Ly outputs), z-forward DFT (Lz = 16, pruned),
+//                real-symmetric 6-component tensor MAC, z-inverse, y-inverse (ny live
+//                outputs) — written back in place. The padded spectrum never reaches HBM.
+//   KXI (k_xi) : x-c2r back to the nx live cells of H_demag (SoA, x fastest).
+//
+// Replaces proj/src/demag.cpp:67-145 (pad, 3 forward FFTs, MAC, 3 inverse FFTs, window
+// extract). 1/(Lx Ly Lz) is folded into the tensor spectrum (tensor_kernels.cu).
+#include <stdexcept>
+#include <string>
+
+#include "fast.hpp"
+#include "fft4.cuh"
+
+namespace mmb {
+
+namespace {
+
+void check_launch() {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+template <int LOG2L>
+constexpr int x_pairs() {
+    constexpr int n2 = Split<LOG2L>::N2;
+    return n2 >= 256 ? 1 : 256 / n2;
+}
+template <typename T, int LOG2L>
+constexpr int x_smem_bytes() {
+    using S = Split<LOG2L>;
+    constexpr int P = x_pairs<LOG2L>();
+    constexpr int ex = P * S::N2 * (S::N1 + 1);
+    constexpr int zz = P * ((1 << LOG2L) + 1);
+    constexpr int rr = 2 * P * (((1 << LOG2L) / 2 + 1) | 1);
+    int m = ex > zz ? ex : zz;
+    m = m > rr ? m : rr;
+    return m * static_cast<int>(sizeof(cx<T>));
+}
+
+__device__ __forceinline__ long long sf_row(int kx, int c, int z, int nz, int ly) {
+    return ((static_cast<long long>(kx) * 3 + c) * nz + z) * ly;
+}
+
+// ------------------------------------------------------------------ KX: x forward
+template <typename T, int LOG2L>
+__global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
+    k_xf(const T* __restrict__ m, cx<T>* __restrict__ S, Geom g, const cx<T>* __restrict__ tw,
+         StepCtl* ctl, StageTable st, int prologue) {
+    using SP = Split<LOG2L>;
+    constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = x_pairs<LOG2L>();
+    constexpr int XH = L == 1 ? 1 : L / 2 + 1;
+    constexpr int EX = N1 + 1, ZP = L + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+    if (prologue && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
+        step_prologue(ctl, st, prologue);
+
+    const int y0 = blockIdx.x * (2 * P), z = blockIdx.y, c = blockIdx.z;
+    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    const int tid = threadIdx.x;
+    const T* plane = m + (static_cast<long long>(c) * nz + z) * ny * nx;
+
+    // stage A: task (p, n1), n1 fastest; inputs beyond nx (and rows beyond ny) are zero
+    if (tid < P * N1) {
+        const int p = tid / N1, n1 = tid % N1;
+        const int ya = y0 + 2 * p, yb = ya + 1;
+        const T* ra = plane + static_cast<long long>(ya) * nx;
+        const T* rb = plane + static_cast<long long>(yb) * nx;
+        const bool va = ya < ny, vb = yb < ny;
+        constexpr int NZ = L == 1 ? 1 : N2 / 2;
+        cx<T> v[N2];
+#pragma unroll
+        for (int n2 = 0; n2 < NZ; ++n2) {
+            const int x = n1 + N1 * n2;
+            const bool in = x < nx;
+            v[n2] = cx<T>{(in && va) ? __ldg(ra + x) : T(0), (in && vb) ? __ldg(rb + x) : T(0)};
+        }
+        DftP<N2, -1, NZ, N2>::run(v);
+        cx<T>* ex = sm + (p * N2) * EX + n1;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+            cx<T> w = v[k2];
+            if (k2 > 0 && n1 > 0) w = cmul(w, __ldg(&tw[n1 * k2]));
+            ex[k2 * EX] = w;
+        }
+    }
+    __syncthreads();
+    // stage B: task (p, k2), k2 fastest -> natural-order Z[k2 + N2 k1]
+    {
+        const int p = tid / N2, k2 = tid % N2;
+        cx<T> u[N1];
+        const cx<T>* ex = sm + (p * N2 + k2) * EX;
+#pragma unroll
+        for (int n1 = 0; n1 < N1; ++n1) u[n1] = ex[n1];
+        DftP<N1, -1, N1, N1>::run(u);
+        __syncthreads();
+        cx<T>* zr = sm + p * ZP + k2;
+#pragma unroll
+        for (int k1 = 0; k1 < N1; ++k1) zr[N2 * k1] = u[k1];
+    }
+    __syncthreads();
+    // separate the packed rows; task (k, r), r fastest -> coalesced kx-major stores
+    const T half = T(0.5);
+    const int ly = g.ly;
+    for (int it = tid; it < XH * 2 * P; it += blockDim.x) {
+        const int r = it % (2 * P), k = it / (2 * P);
+        const int y = y0 + r;
+        if (y >= ny) continue;
+        const cx<T>* zr = sm + (r >> 1) * ZP;
+        const cx<T> zk = zr[k], zm = zr[(L - k) & (L - 1)];
+        const cx<T> val = (r & 1) ? cx<T>{(zk.y + zm.y) * half, (zm.x - zk.x) * half}
+                                  : cx<T>{(zk.x + zm.x) * half, (zk.y - zm.y) * half};
+        S[sf_row(k, c, z, nz, ly) + y] = val;
+    }
+}
+
+// ------------------------------------------------------------------ KXI: x inverse
+template <typename T, int LOG2L>
+__global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
+    k_xi(const cx<T>* __restrict__ S, T* __restrict__ h, Geom g, const cx<T>* __restrict__ tw) {
+    using SP = Split<LOG2L>;
+    constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = x_pairs<LOG2L>();
+    constexpr int XH = L == 1 ? 1 : L / 2 + 1;
+    constexpr int EX = N1 + 1, RP = (L / 2 + 1) | 1; // odd staging pitch: conflict free
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+
+    const int y0 = blockIdx.x * (2 * P), z = blockIdx.y, c = blockIdx.z;
+    const int nx = g.nx, ny = g.ny, nz = g.nz, ly = g.ly;
+    const int tid = threadIdx.x;
+
+    // stage the 2P half-spectrum rows: task (k, r), r fastest (coalesced reads)
+    for (int it = tid; it < XH * 2 * P; it += blockDim.x) {
+        const int r = it % (2 * P), k = it / (2 * P);
+        const int y = y0 + r;
+        sm[r * RP + k] = (y < ny) ? S[sf_row(k, c, z, nz, ly) + y] : cx<T>{0, 0};
+    }
+    __syncthreads();
+    // stage A on Z = A + iB (full circle from the two Hermitian halves)
+    cx<T> v[N2];
+    int p = 0, n1 = 0;
+    const bool a_task = tid < P * N1;
+    if (a_task) {
+        p = tid / N1;
+        n1 = tid % N1;
+        const cx<T>* A = sm + (2 * p) * RP;
+        const cx<T>* B = A + RP;
+#pragma unroll
+        for (int n2 = 0; n2 < N2; ++n2) {
+            const int k = n1 + N1 * n2;
+            cx<T> zv;
+            if (k == 0 || 2 * k == L) {
+                zv = cx<T>{A[k].x, B[k].x};
+            } else if (2 * k < L) {
+                const cx<T> a = A[k], b = B[k];
+                zv = cx<T>{a.x - b.y, a.y + b.x};
+            } else {
+                const cx<T> a = A[L - k], b = B[L - k];
+                zv = cx<T>{a.x + b.y, b.x - a.y};
+            }
+            v[n2] = zv;
+        }
+        DftP<N2, +1, N2, N2>::run(v);
+    }
+    __syncthreads();
+    if (a_task) {
+        cx<T>* ex = sm + (p * N2) * EX + n1;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+            cx<T> w = v[k2];
+            if (k2 > 0 && n1 > 0) w = cmulc(w, __ldg(&tw[n1 * k2]));
+            ex[k2 * EX] = w;
+        }
+    }
+    __syncthreads();
+    // stage B: natural-order outputs, only the nx live cells
+    {
+        const int pb = tid / N2, k2 = tid % N2;
+        cx<T> u[N1];
+        const cx<T>* ex = sm + (pb * N2 + k2) * EX;
+#pragma unroll
+        for (int q = 0; q < N1; ++q) u[q] = ex[q];
+        constexpr int NO = N1 == 1 ? 1 : N1 / 2;
+        DftP<N1, +1, N1, NO>::run(u);
+        const int ya = y0 + 2 * pb, yb = ya + 1;
+        T* ha = h + ((static_cast<long long>(c) * nz + z) * ny + ya) * nx;
+        T* hb = ha + nx;
+#pragma unroll
+        for (int k1 = 0; k1 < NO; ++k1) {
+            const int x = k2 + N2 * k1;
+            if (x < nx) {
+                if (ya < ny) ha[x] = u[k1].x;
+                if (yb < ny) hb[x] = u[k1].y;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ KYZ: y, z, MAC, z^-1, y^-1
+template <int LOG2L>
+constexpr int yz_threads() {
+    constexpr int n2 = Split<LOG2L>::N2;
+    return n2 >= 384 ? n2 : (384 / n2) * n2;
+}
+
+template <typename T, int LOG2L, int ZM>
+__global__ void __launch_bounds__(yz_threads<LOG2L>())
+    k_yz(cx<T>* __restrict__ S, Geom g, const cx<T>* __restrict__ tw, const T* __restrict__ kt,
+         int kxb) {
+    using SP = Split<LOG2L>;
+    constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2;
+    constexpr int RP = fpitch<LOG2L>();
+    constexpr int NT = yz_threads<LOG2L>();
+    constexpr int RB = NT / N2; // rows per batch
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+
+    const int nz = g.nz, ny = g.ny, xh = g.xh;
+    const int kx0 = blockIdx.x * kxb;
+    const int kxn = min(kxb, xh - kx0);
+    const int rows = kxn * 3 * nz;
+    const int tid = threadIdx.x;
+    cx<T>* gblk = S + sf_row(kx0, 0, 0, nz, L); // rows of this CTA are contiguous in S
+
+    // ---- y forward, batches of RB rows
+    for (int rb0 = 0; rb0 < rows; rb0 += RB) {
+        const int nb = min(RB, rows - rb0);
+        cx<T> v[N2];
+        const int ra = rb0 + tid / N1, n1 = tid % N1;
+        const bool a_task = tid < nb * N1;
+        if (a_task) {
+            const cx<T>* src = gblk + static_cast<long long>(ra) * L;
+            constexpr int NZ = L == 1 ? 1 : N2 / 2;
+#pragma unroll
+            for (int n2 = 0; n2 < NZ; ++n2) {
+                const int y = n1 + N1 * n2;
+                v[n2] = y < ny ? src[y] : cx<T>{0, 0};
+            }
+            DftP<N2, -1, NZ, N2>::run(v);
+            cx<T>* dst = sm + ra * RP;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) {
+                cx<T> w = v[k2];
+                if (k2 > 0 && n1 > 0) w = cmul(w, __ldg(&tw[n1 * k2]));
+                dst[fpad<LOG2L>(k2 * N1 + n1)] = w;
+            }
+        }
+        __syncthreads();
+        const int rbr = rb0 + tid / N2, k2 = tid % N2;
+        const bool b_task = tid < nb * N2;
+        cx<T> u[N1];
+        if (b_task) {
+            const cx<T>* src = sm + rbr * RP;
+#pragma unroll
+            for (int q = 0; q < N1; ++q) u[q] = src[fpad<LOG2L>(k2 * N1 + q)];
+            DftP<N1, -1, N1, N1>::run(u);
+        }
+        __syncthreads();
+        if (b_task) {
+            cx<T>* dst = sm + rbr * RP;
+#pragma unroll
+            for (int k1 = 0; k1 < N1; ++k1) dst[fpad<LOG2L>(k2 + N2 * k1)] = u[k1];
+        }
+    }
+    __syncthreads();
+
+    // ---- z forward + tensor MAC + z inverse, one pencil (kx, ky) per task
+    {
+        const int ly = L, yh = g.yh, zh = g.zh;
+        for (int it = tid; it < kxn * ly; it += NT) {
+            const int kxl = it / ly, ky = it % ly;
+            const int kx = kx0 + kxl;
+            const bool fy = 2 * ky > ly;
+            const int kyo = fy ? ly - ky : ky;
+            const T* kb = kt + static_cast<long long>(kx) * 6 * zh * yh + kyo;
+            cx<T>* base = sm + (kxl * 3 * nz) * RP + fpad<LOG2L>(ky);
+            if constexpr (ZM == 0) {
+                // nz == 1: MAC only
+                cx<T> a = base[0], b = base[RP], cc = base[2 * RP];
+                T k6[6];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) k6[q] = __ldg(kb + q * yh);
+                if (fy) {
+                    k6[1] = -k6[1];
+                    k6[4] = -k6[4];
+                }
+                mac3<T>(k6, a, b, cc);
+                base[0] = a;
+                base[RP] = b;
+                base[2 * RP] = cc;
+            } else {
+                // 2 <= nz <= 8, Lz = 16
+                cx<T> w[3][16];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+#pragma unroll
+                    for (int zz = 0; zz < 8; ++zz)
+                        w[c][zz] = zz < nz ? base[(c * nz + zz) * RP] : cx<T>{0, 0};
+                    DftP<16, -1, 8, 16>::run(w[c]);
+                }
+#pragma unroll
+                for (int kzo = 0; kzo <= 8; ++kzo) {
+                    T k6[6];
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) k6[q] = __ldg(kb + (q * zh + kzo) * yh);
+                    if (fy) {
+                        k6[1] = -k6[1];
+                        k6[4] = -k6[4];
+                    }
+                    mac3<T>(k6, w[0][kzo], w[1][kzo], w[2][kzo]);
+                    if (kzo != 0 && kzo != 8) {
+                        // kz = 16 - kzo: xz and yz are odd in z
+                        k6[2] = -k6[2];
+                        k6[4] = -k6[4];
+                        mac3<T>(k6, w[0][16 - kzo], w[1][16 - kzo], w[2][16 - kzo]);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    DftP<16, +1, 16, 8>::run(w[c]);
+#pragma unroll
+                    for (int zz = 0; zz < 8; ++zz)
+                        if (zz < nz) base[(c * nz + zz) * RP] = w[c][zz];
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- y inverse, batches of RB rows, ny live outputs straight to HBM
+    for (int rb0 = 0; rb0 < rows; rb0 += RB) {
+        const int nb = min(RB, rows - rb0);
+        cx<T> v[N2];
+        const int ra = rb0 + tid / N1, n1 = tid % N1;
+        const bool a_task = tid < nb * N1;
+        if (a_task) {
+            const cx<T>* src = sm + ra * RP;
+#pragma unroll
+            for (int n2 = 0; n2 < N2; ++n2) v[n2] = src[fpad<LOG2L>(n1 + N1 * n2)];
+            DftP<N2, +1, N2, N2>::run(v);
+        }
+        __syncthreads();
+        if (a_task) {
+            cx<T>* dst = sm + ra * RP;
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) {
+                cx<T> w = v[k2];
+                if (k2 > 0 && n1 > 0) w = cmulc(w, __ldg(&tw[n1 * k2]));
+                dst[fpad<LOG2L>(k2 * N1 + n1)] = w;
+            }
+        }
+        __syncthreads();
+        const int rbr = rb0 + tid / N2, k2 = tid % N2;
+        if (tid < nb * N2) {
+            cx<T> u[N1];
+            const cx<T>* src = sm + rbr * RP;
+#pragma unroll
+            for (int q = 0; q < N1; ++q) u[q] = src[fpad<LOG2L>(k2 * N1 + q)];
+            constexpr int NO = N1 == 1 ? 1 : N1 / 2;
+            DftP<N1, +1, N1, NO>::run(u);
+            cx<T>* dst = gblk + static_cast<long long>(rbr) * L;
+#pragma unroll
+            for (int k1 = 0; k1 < NO; ++k1) {
+                const int y = k2 + N2 * k1;
+                if (y < ny) dst[y] = u[k1];
+            }
+        }
+    }
+}
+
+template <typename K>
+void set_smem(K kernel, int bytes) {
+    if (bytes > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    }
+}
+
+#define MMB_FAST_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12)
+
+} // namespace
+
+template <typename T>
+int fast_yz_kxb(const Geom& g, int* smem_bytes) {
+    // kx per CTA: fill ~100 KB (two CTAs per SM) when possible, else one block of up to
+    // the 227 KB opt-in limit.
+    const int rowbytes = [&] {
+        switch (g.log2ly) {
+#define X(l) case l: return fpitch<l>() * static_cast<int>(sizeof(cx<T>));
+            MMB_FAST_CASES(X)
+#undef X
+            default: return 0;
+        }
+    }();
+    if (!rowbytes) return 0;
+    const int per_kx = 3 * g.nz * rowbytes;
+    const int limit = 220 * 1024;
+    if (per_kx > limit) return 0;
+    int kxb = (100 * 1024) / per_kx;
+    if (kxb < 1) kxb = 1;
+    kxb = std::min(kxb, 64);
+    kxb = std::min(kxb, g.xh);
+    if (smem_bytes) *smem_bytes = kxb * per_kx;
+    return kxb;
+}
+
+template <typename T>
+bool fast_supported(const Geom& g) {
+    if (g.lx < 2 || g.ly < 2) return false;
+    if (g.log2lx > 12 || g.log2ly > 12) return false;
+    if (sizeof(T) == 8 && (g.log2lx > 11 || g.log2ly > 11)) return false; // DFT_64 f64 spills
+    if (g.nz > 8) return false;
+    if (sizeof(T) == 8 && g.nz > 1) return false; // 3 x 16 complex f64 pencils would spill
+    if (g.nz > 1 && g.lz != 16) return false;
+    return fast_yz_kxb<T>(g, nullptr) > 0;
+}
+
+template <typename T>
+void prepare_fast_kernels(const Geom& g) {
+    switch (g.log2lx) {
+#define X(l) case l: set_smem(k_xf<T, l>, x_smem_bytes<T, l>()); set_smem(k_xi<T, l>, x_smem_bytes<T, l>()); break;
+        MMB_FAST_CASES(X)
+#undef X
+        default: throw std::invalid_argument("fast path: bad Lx");
+    }
+    int sb = 0;
+    fast_yz_kxb<T>(g, &sb);
+    switch (g.log2ly) {
+#define X(l) case l: set_smem(k_yz<T, l, 0>, sb); if constexpr (sizeof(T) == 4) set_smem(k_yz<T, l, 1>, sb); break;
+        MMB_FAST_CASES(X)
+#undef X
+        default: throw std::invalid_argument("fast path: bad Ly");
+    }
+}
+
+template <typename T>
+void launch_fast_xf(const T* m, cx<T>* S, const Geom& g, const cx<T>* tw, StepCtl* ctl,
+                    const StageTable& st, int prologue, cudaStream_t stream) {
+    switch (g.log2lx) {
+#define X(l) case l: { constexpr int P = x_pairs<l>(); \
+        const dim3 grid((g.ny + 2 * P - 1) / (2 * P), g.nz, 3); \
+        k_xf<T, l><<<grid, P * Split<l>::N2, x_smem_bytes<T, l>(), stream>>>(m, S, g, tw, ctl, st, prologue); break; }
+        MMB_FAST_CASES(X)
+#undef X
+        default: throw std::invalid_argument("fast path: bad Lx");
+    }
+    check_launch();
+}
+
+template <typename T>
+void launch_fast_xi(const cx<T>* S, T* h, const Geom& g, const cx<T>* tw, cudaStream_t stream) {
+    switch (g.log2lx) {
+#define X(l) case l: { constexpr int P = x_pairs<l>(); \
+        const dim3 grid((g.ny + 2 * P - 1) / (2 * P), g.nz, 3); \
+        k_xi<T, l><<<grid, P * Split<l>::N2, x_smem_bytes<T, l>(), stream>>>(S, h, g, tw); break; }
+        MMB_FAST_CASES(X)
+#undef X
+        default: throw std::invalid_argument("fast path: bad Lx");
+    }
+    check_launch();
+}
+
+template <typename T>
+void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, cudaStream_t stream) {
+    int sb = 0;
+    const int kxb = fast_yz_kxb<T>(g, &sb);
+    const unsigned grid = static_cast<unsigned>((g.xh + kxb - 1) / kxb);
+    switch (g.log2ly) {
+#define X(l) case l: \
+        if (g.nz == 1) k_yz<T, l, 0><<<grid, yz_threads<l>(), sb, stream>>>(S, g, tw, kt, kxb); \
+        else if constexpr (sizeof(T) == 4) k_yz<T, l, 1><<<grid, yz_threads<l>(), sb, stream>>>(S, g, tw, kt, kxb); \
+        else throw std::invalid_argument("fast path: f64 needs nz == 1"); break;
+        MMB_FAST_CASES(X)
+#undef X
+        default: throw std::invalid_argument("fast path: bad Ly");
+    }
+    check_launch();
+}
+
+#define MMB_FINST(T)                                                                            \
+    template int fast_yz_kxb<T>(const Geom&, int*);                                            \
+    template bool fast_supported<T>(const Geom&);                                              \
+    template void prepare_fast_kernels<T>(const Geom&);                                        \
+    template void launch_fast_xf<T>(const T*, cx<T>*, const Geom&, const cx<T>*, StepCtl*,      \
+                                    const StageTable&, int, cudaStream_t);                     \
+    template void launch_fast_xi<T>(const cx<T>*, T*, const Geom&, const cx<T>*, cudaStream_t); \
+    template void launch_fast_yz<T>(cx<T>*, const Geom&, const cx<T>*, const T*, cudaStream_t);
+#ifndef MMB_ONLY_F64
+MMB_FINST(float)
+#endif
+#ifndef MMB_ONLY_F32
+MMB_FINST(double)
+#endif
+
+} // namespace mmb

@@ -1,0 +1,80 @@
+// fft4.cuh — register-resident pruned DFTs and the two-stage ("four-step") line FFT used by
+// the fast path.
+//
+// A length L = N1*N2 transform is done as: stage A, one task per n1 < N1 computes
+// DFT_N2 over x[n1 + N1*n2] in registers and multiplies by W_L^{n1*k2}; one exchange
+// through shared memory; stage B, one task per k2 < N2 computes DFT_N1 over n1, giving
+// X[k2 + N2*k1] in natural order. Loads in stage A and stores in stage B are unit-stride
+// across consecutive tasks (coalesced in global memory, conflict-free in shared memory),
+// so a line FFT costs one shared-memory round trip.
+//
+// Pruning: the demag convolution's forward inputs are zero beyond the live cells
+// (n >= L/2) and its inverse outputs are only needed below them, so DftP takes the number
+// of leading non-zero inputs (NZ) and of leading outputs needed (NO) as compile-time
+// bounds and drops the butterflies that only touch zeros or unused outputs.
+#pragma once
+
+#include "common.cuh"
+
+namespace mmb {
+
+template <int LOG2L> struct Split {
+    static constexpr int L = 1 << LOG2L;
+    static constexpr int N2 = 1 << ((LOG2L + 1) / 2); // stage-A DFT size (>= N1)
+    static constexpr int N1 = L / N2;                 // stage-B DFT size
+    static constexpr int LOG2N1 = LOG2L / 2;
+};
+
+// Pruned radix-2 DIT DFT on registers: v[0..R) in natural order -> natural order.
+// Inputs v[NZ..R) are treated as zero (never read); outputs >= NO are left undefined.
+template <int R, int SIGN, int NZ = R, int NO = R>
+struct DftP {
+    template <typename C>
+    static __device__ __forceinline__ void run(C* v) {
+        if constexpr (R == 1) {
+            if constexpr (NZ == 0) v[0] = C{0, 0};
+        } else if constexpr (NZ == 0) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) v[k] = C{0, 0};
+        } else if constexpr (NZ == 1) {
+#pragma unroll
+            for (int k = 1; k < R; ++k)
+                if (k < NO) v[k] = v[0];
+        } else {
+            constexpr int H = R / 2;
+            constexpr int NOH = NO < H ? NO : H;
+            C e[H], o[H];
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+                e[i] = (2 * i < NZ) ? v[2 * i] : C{0, 0};
+                o[i] = (2 * i + 1 < NZ) ? v[2 * i + 1] : C{0, 0};
+            }
+            DftP<H, SIGN, (NZ + 1) / 2, NOH>::run(e);
+            DftP<H, SIGN, NZ / 2, NOH>::run(o);
+            combine<0>(v, e, o);
+        }
+    }
+    template <int K, typename C>
+    static __device__ __forceinline__ void combine(C* v, const C* e, const C* o) {
+        constexpr int H = R / 2;
+        if constexpr (K < H && K < NO) {
+            const C t = rot64<K * (64 / R), SIGN>(o[K]);
+            v[K] = cadd(e[K], t);
+            if constexpr (K + H < NO) v[K + H] = csub(e[K], t);
+            combine<K + 1>(v, e, o);
+        }
+    }
+};
+
+// Smem index padding for a row of length L = N1*N2 processed by the four-step: one slot
+// per N1 elements, so stage-B reads at stride N1 become stride N1+1 (conflict free).
+template <int LOG2L>
+__device__ __forceinline__ int fpad(int i) {
+    return i + (i >> Split<LOG2L>::LOG2N1);
+}
+template <int LOG2L>
+__host__ __device__ constexpr int fpitch() {
+    return (1 << LOG2L) + Split<LOG2L>::N2;
+}
+
+} // namespace mmb

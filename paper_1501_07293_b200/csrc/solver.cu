@@ -9,6 +9,7 @@
 // contract (exceptions mapped to status codes as proj/src/capi.cpp:31-58 does).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -17,6 +18,7 @@
 #include <vector>
 
 #include "../../include/mmb.h"
+#include "fast.hpp"
 #include "kernels.hpp"
 
 namespace mmb {
@@ -122,12 +124,15 @@ public:
         g.n = static_cast<long long>(d.nx) * d.ny * d.nz;
         g.rows = static_cast<long long>(d.ny) * d.nz;
 
+        const char* force_general = std::getenv("MMB_GENERAL_PATH");
+        fast_ = fast_supported<T>(g) && !(force_general && force_general[0] == '1');
+
         const size_t n = static_cast<size_t>(g.n);
         m_[0].alloc(3 * n);
         m_[1].alloc(3 * n);
         hd_.alloc(3 * n);
         heff_.alloc(3 * n);
-        S_.alloc(static_cast<size_t>(3) * g.nz * g.ly * g.xp);
+        S_.alloc(static_cast<size_t>(3) * g.nz * g.ly * (fast_ ? g.xh : g.xp));
         kspec_.alloc(static_cast<size_t>(6) * g.zh * g.yh * g.xh);
         twx_.alloc(g.lx);
         twy_.alloc(g.ly);
@@ -140,7 +145,8 @@ public:
         launch_twiddles<T>(twx_.p, g.lx, stream_);
         launch_twiddles<T>(twy_.p, g.ly, stream_);
         launch_twiddles<T>(twz_.p, g.lz, stream_);
-        prepare_fft_kernels<T>(g_);
+        if (fast_) prepare_fast_kernels<T>(g_);
+        else prepare_fft_kernels<T>(g_);
 
         // StepCtl: step 0, alpha from the material (llg.cpp:31-33).
         StepCtl c{};
@@ -420,11 +426,13 @@ private:
         a3.alloc(6 * c3);
         launch_axis_transform(a2.p, a3.p, g.xh, g.yh, g.nz, 2, g.lz, csz.p, 0x14, c2, c3, stream_);
         const double scale = 1.0 / (static_cast<double>(g.lx) * g.ly * g.lz);
-        launch_tensor_finalize<T>(a3.p, kspec_.p, c3, scale, stream_);
+        if (fast_) launch_tensor_finalize_fast<T>(a3.p, kspec_.p, g.xh, g.yh, g.zh, scale, stream_);
+        else launch_tensor_finalize<T>(a3.p, kspec_.p, c3, scale, stream_);
         ck(cudaStreamSynchronize(stream_), "spectrum sync");
     }
 
     std::vector<std::string> kernel_names() const {
+        if (fast_) return {"x_fwd", "yz", "x_inv", "llg"};
         if (g_.nz == 1) return {"x_fwd", "y_mac", "x_inv", "llg"};
         return {"x_fwd", "y_fwd", "z_mac", "y_inv", "x_inv", "llg"};
     }
@@ -435,6 +443,15 @@ private:
         auto mark = [&]() {
             if (ev) ck(cudaEventRecord(ev[k++], stream_), "record");
         };
+        if (fast_) {
+            launch_fast_xf<T>(m, S_.p, g_, twx_.p, ctl_.p, st_, prologue, stream_);
+            mark();
+            launch_fast_yz<T>(S_.p, g_, twy_.p, kspec_.p, stream_);
+            mark();
+            launch_fast_xi<T>(S_.p, h, g_, twx_.p, stream_);
+            mark();
+            return;
+        }
         launch_x_fwd<T>(m, S_.p, g_, twx_.p, ctl_.p, st_, prologue, stream_);
         mark();
         if (g_.nz == 1) {
@@ -518,6 +535,7 @@ private:
     StepCtl* ctl_host_ = nullptr;
     cudaGraphExec_t graph_[2] = {nullptr, nullptr};
     int cur_ = 0;
+    bool fast_ = false;
     long long step_ = 0;
     double exch_coeff_ = 0.0, aniso_coeff_ = 0.0;
 };

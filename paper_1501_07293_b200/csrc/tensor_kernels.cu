@@ -11,6 +11,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "fast.hpp"
 #include "kernels.hpp"
 
 namespace mmb {
@@ -85,6 +86,22 @@ __global__ void k_finalize(const double* __restrict__ spec, T* __restrict__ out,
     out[c * count + f] = static_cast<T>(sgn * scale * spec[c * count + f]);
 }
 
+// Fast-path layout [kx][c][kz][ky] (ky fastest): one contiguous tensor slab per kx.
+template <typename T>
+__global__ void k_finalize_fast(const double* __restrict__ spec, T* __restrict__ out, int xh, int yh,
+                                int zh, double scale) {
+    const long long count = static_cast<long long>(xh) * yh * zh;
+    const long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (f >= count) return;
+    const int c = blockIdx.y;
+    const int kx = static_cast<int>(f % xh);
+    const long long r = f / xh;
+    const int ky = static_cast<int>(r % yh), kz = static_cast<int>(r / yh);
+    const double sgn = (c == 1 || c == 2 || c == 4) ? -1.0 : 1.0;
+    out[((static_cast<long long>(kx) * 6 + c) * zh + kz) * yh + ky] =
+        static_cast<T>(sgn * scale * spec[c * count + f]);
+}
+
 // W_L^t = exp(-2 pi i t / L), fp64 sincospi then narrowed.
 template <typename T>
 __global__ void k_twiddles(cx<T>* tw, int L) {
@@ -123,6 +140,15 @@ void launch_tensor_finalize(const double* spec, T* out, long long count, double 
 }
 
 template <typename T>
+void launch_tensor_finalize_fast(const double* spec, T* out, int xh, int yh, int zh, double scale,
+                                 cudaStream_t stream) {
+    const long long count = static_cast<long long>(xh) * yh * zh;
+    const dim3 grid(static_cast<unsigned>((count + 255) / 256), 6);
+    k_finalize_fast<T><<<grid, 256, 0, stream>>>(spec, out, xh, yh, zh, scale);
+    check_launch();
+}
+
+template <typename T>
 void launch_twiddles(cx<T>* tw, int L, cudaStream_t stream) {
     k_twiddles<T><<<(L + 255) / 256, 256, 0, stream>>>(tw, L);
     check_launch();
@@ -130,6 +156,8 @@ void launch_twiddles(cx<T>* tw, int L, cudaStream_t stream) {
 
 template void launch_tensor_finalize<float>(const double*, float*, long long, double, cudaStream_t);
 template void launch_tensor_finalize<double>(const double*, double*, long long, double, cudaStream_t);
+template void launch_tensor_finalize_fast<float>(const double*, float*, int, int, int, double, cudaStream_t);
+template void launch_tensor_finalize_fast<double>(const double*, double*, int, int, int, double, cudaStream_t);
 template void launch_twiddles<float>(cx<float>*, int, cudaStream_t);
 template void launch_twiddles<double>(cx<double>*, int, cudaStream_t);
 

@@ -23,6 +23,16 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = os.path.join(HERE, "golden")
 TOL_H = {"f64": 1e-12, "f32": 1e-5}
 
+
+@pytest.fixture(params=["fast", "general"])
+def path(request, monkeypatch):
+    """Both demag paths: the fused fast path (where supported) and the general pipeline."""
+    if request.param == "general":
+        monkeypatch.setenv("MMB_GENERAL_PATH", "1")
+    else:
+        monkeypatch.delenv("MMB_GENERAL_PATH", raising=False)
+    return request.param
+
 GRIDS = [
     (1, 1, 1, 2.0), (2, 2, 2, 1.0), (3, 3, 3, 2.0), (4, 4, 2, 1.0), (5, 3, 2, 3.0), (7, 1, 1, 1.0),
     (1, 6, 2, 1.0), (8, 8, 4, 1.0), (6, 5, 3, 1.0), (16, 12, 3, 2.5), (33, 17, 1, 3.0),
@@ -41,7 +51,7 @@ def test_tensor_entries_match_reference(refsolver, grid):
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
 @pytest.mark.parametrize("grid", GRIDS)
-def test_demag_field_matches_reference(refsolver, grid, prec):
+def test_demag_field_matches_reference(refsolver, grid, prec, path):
     nx, ny, nz, delta = grid
     dt = np.float64 if prec == "f64" else np.float32
     sp = spec(nx, ny, nz, delta)
@@ -68,7 +78,7 @@ def test_demag_fft_vs_direct_sum(refsolver, prec):
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-def test_effective_field_matches_golden(prec):
+def test_effective_field_matches_golden(prec, path):
     d = np.load(os.path.join(GOLD, "fields_small.npz"))
     for idx, row in enumerate(d["cases"]):
         nx, ny, nz = int(row[0]), int(row[1]), int(row[2])
@@ -86,7 +96,7 @@ def test_effective_field_matches_golden(prec):
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
 @pytest.mark.parametrize("grid", [(16, 12, 3, 2.5), (40, 24, 9, 2.0), (166, 42, 1, 3.0), (64, 64, 1, 1.0)])
-def test_steps_match_reference(refsolver, grid, prec):
+def test_steps_match_reference(refsolver, grid, prec, path):
     nx, ny, nz, delta = grid
     dt = np.float64 if prec == "f64" else np.float32
     sp = spec(nx, ny, nz, delta, 1.3e7, 800.0, 30.0, 0.5, 5e-6,
@@ -226,7 +236,7 @@ def _crossing(rows, reversal=50000, dt=5e-6):
     ("sp4_166_f64", (166, 42, 3.0), "f64"), ("sp4_128_f64", (128, 32, 3.90625), "f64"),
     ("sp4_166_f32", (166, 42, 3.0), "f32"), ("sp4_128_f32", (128, 32, 3.90625), "f32"),
 ])
-def test_sp4_trajectory_matches_reference(name, grid, prec):
+def test_sp4_trajectory_matches_reference(name, grid, prec, path):
     want = _load_traj(name)
     sim = b200(sp4(*grid), prec)
     recs = []
@@ -248,7 +258,7 @@ def test_sp4_trajectory_matches_reference(name, grid, prec):
 
 
 # ---------------------------------------------------------------- full-size properties
-def test_512x512x8_f32_properties():
+def test_512x512x8_f32_properties(path):
     sp = spec(512, 512, 8, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5)
     sim = b200(sp, "f32")
     rng = np.random.default_rng(5)
