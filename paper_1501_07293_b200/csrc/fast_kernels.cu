@@ -41,11 +41,27 @@ constexpr int x_smem_bytes() {
     constexpr int rr = 2 * P * (((1 << LOG2L) / 2 + 1) | 1);
     int m = ex > zz ? ex : zz;
     m = m > rr ? m : rr;
-    return m * static_cast<int>(sizeof(cx<T>));
+    return (m + (1 << LOG2L)) * static_cast<int>(sizeof(cx<T>)); // + twiddle table
+}
+template <typename T, int LOG2L>
+constexpr int x_main_words() {
+    return x_smem_bytes<T, LOG2L>() / static_cast<int>(sizeof(cx<T>)) - (1 << LOG2L);
 }
 
-__device__ __forceinline__ long long sf_row(int kx, int c, int z, int nz, int ly) {
-    return ((static_cast<long long>(kx) * 3 + c) * nz + z) * ly;
+// S row (kx, c, z) start; rows hold the ny live y values (the padded half never reaches HBM)
+__device__ __forceinline__ long long sf_row(int kx, int c, int z, int nz, int ny) {
+    return ((static_cast<long long>(kx) * 3 + c) * nz + z) * ny;
+}
+
+// Stage-A twiddles W_L^{n1*k2} staged in shared memory as [k2][n1] (unit stride across the
+// n1-consecutive lanes of stage A: bank-conflict free, no global loads on the hot path).
+template <typename T, int LOG2L>
+__device__ __forceinline__ void stage_twiddles(cx<T>* tws, const cx<T>* __restrict__ tw) {
+    using SP = Split<LOG2L>;
+    for (int e = threadIdx.x; e < SP::L; e += blockDim.x) {
+        const int k2 = e / SP::N1, n1 = e % SP::N1;
+        tws[e] = __ldg(&tw[n1 * k2]);
+    }
 }
 
 // ------------------------------------------------------------------ KX: x forward
@@ -59,8 +75,11 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
     constexpr int EX = N1 + 1, ZP = L + 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+    cx<T>* tws = sm + x_main_words<T, LOG2L>();
     if (prologue && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
         step_prologue(ctl, st, prologue);
+    stage_twiddles<T, LOG2L>(tws, tw);
+    __syncthreads();
 
     const int y0 = blockIdx.x * (2 * P), z = blockIdx.y, c = blockIdx.z;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
@@ -87,7 +106,7 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
 #pragma unroll
         for (int k2 = 0; k2 < N2; ++k2) {
             cx<T> w = v[k2];
-            if (k2 > 0 && n1 > 0) w = cmul(w, __ldg(&tw[n1 * k2]));
+            if (k2 > 0) w = cmul(w, tws[k2 * N1 + n1]);
             ex[k2 * EX] = w;
         }
     }
@@ -117,7 +136,7 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
         const cx<T> zk = zr[k], zm = zr[(L - k) & (L - 1)];
         const cx<T> val = (r & 1) ? cx<T>{(zk.y + zm.y) * half, (zm.x - zk.x) * half}
                                   : cx<T>{(zk.x + zm.x) * half, (zk.y - zm.y) * half};
-        S[sf_row(k, c, z, nz, ly) + y] = val;
+        S[sf_row(k, c, z, nz, ny) + y] = val;
     }
 }
 
@@ -131,16 +150,18 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
     constexpr int EX = N1 + 1, RP = (L / 2 + 1) | 1; // odd staging pitch: conflict free
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+    cx<T>* tws = sm + x_main_words<T, LOG2L>();
 
     const int y0 = blockIdx.x * (2 * P), z = blockIdx.y, c = blockIdx.z;
-    const int nx = g.nx, ny = g.ny, nz = g.nz, ly = g.ly;
+    const int nx = g.nx, ny = g.ny, nz = g.nz;
     const int tid = threadIdx.x;
+    stage_twiddles<T, LOG2L>(tws, tw);
 
     // stage the 2P half-spectrum rows: task (k, r), r fastest (coalesced reads)
     for (int it = tid; it < XH * 2 * P; it += blockDim.x) {
         const int r = it % (2 * P), k = it / (2 * P);
         const int y = y0 + r;
-        sm[r * RP + k] = (y < ny) ? S[sf_row(k, c, z, nz, ly) + y] : cx<T>{0, 0};
+        sm[r * RP + k] = (y < ny) ? S[sf_row(k, c, z, nz, ny) + y] : cx<T>{0, 0};
     }
     __syncthreads();
     // stage A on Z = A + iB (full circle from the two Hermitian halves)
@@ -175,7 +196,7 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
 #pragma unroll
         for (int k2 = 0; k2 < N2; ++k2) {
             cx<T> w = v[k2];
-            if (k2 > 0 && n1 > 0) w = cmulc(w, __ldg(&tw[n1 * k2]));
+            if (k2 > 0) w = cmulc(w, tws[k2 * N1 + n1]);
             ex[k2 * EX] = w;
         }
     }
@@ -223,11 +244,14 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
     cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
 
     const int nz = g.nz, ny = g.ny, xh = g.xh;
+    cx<T>* tws = sm + kxb * 3 * nz * RP;
+    stage_twiddles<T, LOG2L>(tws, tw);
+    __syncthreads();
     const int kx0 = blockIdx.x * kxb;
     const int kxn = min(kxb, xh - kx0);
     const int rows = kxn * 3 * nz;
     const int tid = threadIdx.x;
-    cx<T>* gblk = S + sf_row(kx0, 0, 0, nz, L); // rows of this CTA are contiguous in S
+    cx<T>* gblk = S + sf_row(kx0, 0, 0, nz, ny); // rows of this CTA are contiguous in S
 
     // ---- y forward, batches of RB rows
     for (int rb0 = 0; rb0 < rows; rb0 += RB) {
@@ -236,7 +260,7 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
         const int ra = rb0 + tid / N1, n1 = tid % N1;
         const bool a_task = tid < nb * N1;
         if (a_task) {
-            const cx<T>* src = gblk + static_cast<long long>(ra) * L;
+            const cx<T>* src = gblk + static_cast<long long>(ra) * ny;
             constexpr int NZ = L == 1 ? 1 : N2 / 2;
 #pragma unroll
             for (int n2 = 0; n2 < NZ; ++n2) {
@@ -248,7 +272,7 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) {
                 cx<T> w = v[k2];
-                if (k2 > 0 && n1 > 0) w = cmul(w, __ldg(&tw[n1 * k2]));
+                if (k2 > 0) w = cmul(w, tws[k2 * N1 + n1]);
                 dst[fpad<LOG2L>(k2 * N1 + n1)] = w;
             }
         }
@@ -352,7 +376,7 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) {
                 cx<T> w = v[k2];
-                if (k2 > 0 && n1 > 0) w = cmulc(w, __ldg(&tw[n1 * k2]));
+                if (k2 > 0) w = cmulc(w, tws[k2 * N1 + n1]);
                 dst[fpad<LOG2L>(k2 * N1 + n1)] = w;
             }
         }
@@ -365,7 +389,7 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
             for (int q = 0; q < N1; ++q) u[q] = src[fpad<LOG2L>(k2 * N1 + q)];
             constexpr int NO = N1 == 1 ? 1 : N1 / 2;
             DftP<N1, +1, N1, NO>::run(u);
-            cx<T>* dst = gblk + static_cast<long long>(rbr) * L;
+            cx<T>* dst = gblk + static_cast<long long>(rbr) * ny;
 #pragma unroll
             for (int k1 = 0; k1 < NO; ++k1) {
                 const int y = k2 + N2 * k1;
@@ -401,13 +425,14 @@ int fast_yz_kxb(const Geom& g, int* smem_bytes) {
     }();
     if (!rowbytes) return 0;
     const int per_kx = 3 * g.nz * rowbytes;
-    const int limit = 220 * 1024;
+    const int twb = g.ly * static_cast<int>(sizeof(cx<T>));
+    const int limit = 227 * 1024 - twb;
     if (per_kx > limit) return 0;
     int kxb = (100 * 1024) / per_kx;
     if (kxb < 1) kxb = 1;
     kxb = std::min(kxb, 64);
     kxb = std::min(kxb, g.xh);
-    if (smem_bytes) *smem_bytes = kxb * per_kx;
+    if (smem_bytes) *smem_bytes = kxb * per_kx + twb;
     return kxb;
 }
 

@@ -36,7 +36,11 @@ void prepare_fft_kernels(const Geom& g);
 // mode 1: write H_eff only (m_out receives H_eff), no state change.
 template <typename T>
 void launch_llg(int mode, const T* m, const T* hd, T* out, const Geom& g, double exch_coeff,
-                double aniso_coeff, StepCtl* ctl, cudaStream_t stream);
+                double aniso_coeff, StepCtl* ctl, double* tpart, cudaStream_t stream);
+// CTAs of launch_llg (size of its per-CTA torque partial array) and their reduction into
+// ctl->torque_sq_bits.
+int llg_blocks(const Geom& g);
+void launch_torque_partials(const double* tpart, int nb, StepCtl* ctl, cudaStream_t stream);
 // Deterministic fp64 sums of M components: partial[nblk*3] then out[3] (sum, not mean).
 template <typename T>
 void launch_sum3(const T* m, long long n, double* partial, double* out, cudaStream_t stream);

@@ -11,7 +11,7 @@ namespace mmb {
 
 namespace {
 
-constexpr int kLlgThreads = 256;
+constexpr int kTileX = 32, kTileY = 8, kLlgThreads = kTileX * kTileY;
 constexpr int kRedThreads = 256;
 constexpr int kRedBlocks = 592; // 4 x 148 SMs; fixed so the reduction order is deterministic
 
@@ -47,85 +47,141 @@ __device__ __forceinline__ T exch_sum(const T* __restrict__ src, long long f, in
     return sum;
 }
 
-// K6: one thread per cell.
-//   H = H_demag; H += coeff * exch_sum (local_fields.cpp:39); Hx += (hk/ms) Mx
-//   (local_fields.hpp:28-31); H += applied (local_fields.hpp:43-55)
+// K6: fused local terms + Euler + renormalisation, 2.5-D blocked: each CTA owns a 32 x 8
+// (x, y) column and marches through z; the current plane's tile (+1-cell halo) of M is
+// staged in shared memory for the x/y neighbours, the z neighbours ride in registers. M and
+// H_demag are read once and M_{t+1} written once (ping-pong buffers).
+//   H = H_demag; H += coeff * exch_sum (local_fields.cpp:39; neighbour order -x,+x,-y,+y,
+//   -z,+z with Neumann skips, :27-38); Hx += (hk/ms) Mx (local_fields.hpp:28-31);
+//   H += applied (local_fields.hpp:43-55)
 //   T = M x H; dM = p1 T + p2 (M x T); M += dM (llg.cpp:82-93); max |T|^2 in fp64 (:89-90)
 //   mag = sqrt(Mx^2 + My^2 + Mz^2); M *= T(ms)/mag (vector_field.hpp:56-76)
-// MODE 1 writes H_eff instead (field assembly only).
+// MODE 1 writes H_eff instead (field assembly only). Per-CTA torque maxima go to tpart[]
+// (reduced on demand), so the hot path has no same-address atomics.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kLlgThreads) k_llg(const T* __restrict__ m, const T* __restrict__ hd,
                                                      T* __restrict__ out, Geom g, T coeff, T kan,
-                                                     StepCtl* ctl) {
+                                                     StepCtl* ctl, double* __restrict__ tpart) {
+    constexpr int TW = kTileX + 2, TH = kTileY + 2;
+    __shared__ T tile[3][TH][TW];
     const long long n = g.n;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
-    const long long sy = nx, sz = static_cast<long long>(nx) * ny;
+    const long long sz = static_cast<long long>(nx) * ny;
     const T ax = static_cast<T>(ctl->field[0]);
     const T ay = static_cast<T>(ctl->field[1]);
     const T az = static_cast<T>(ctl->field[2]);
     const T p1 = static_cast<T>(ctl->p1);
     const T p2 = static_cast<T>(ctl->p2);
     const T ms = static_cast<T>(ctl->ms);
-    const long long cur = ctl->cur_step;
-    if (MODE == 0 && blockIdx.x == 0 && threadIdx.x == 0) ctl->step = cur + 1;
+    const long long cur_step = ctl->cur_step;
+    const int tx = threadIdx.x, ty = threadIdx.y, lt = ty * kTileX + tx;
+    if (MODE == 0 && blockIdx.x == 0 && blockIdx.y == 0 && lt == 0) ctl->step = cur_step + 1;
 
+    const int i0 = blockIdx.x * kTileX, j0 = blockIdx.y * kTileY;
+    const int i = i0 + tx, j = j0 + ty;
+    const bool live = i < nx && j < ny;
+    const long long oxy = static_cast<long long>(j) * nx + i;
+    T prv[3] = {T(0), T(0), T(0)}, cur[3], nxt[3] = {T(0), T(0), T(0)};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) cur[c] = live ? __ldg(m + c * n + oxy) : T(0);
     double tmax = 0.0;
-    const long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (f < n) {
-        const int i = static_cast<int>(f % nx);
-        const long long r = f / nx;
-        const int j = static_cast<int>(r % ny);
-        const int k = static_cast<int>(r / ny);
-        const T* mxp = m;
-        const T* myp = m + n;
-        const T* mzp = m + 2 * n;
-        const T mx = __ldg(mxp + f), my = __ldg(myp + f), mz = __ldg(mzp + f);
-        T hx = __ldg(hd + f), hy = __ldg(hd + n + f), hz = __ldg(hd + 2 * n + f);
-        hx += coeff * exch_sum(mxp, f, i, j, k, nx, ny, nz, sy, sz);
-        hy += coeff * exch_sum(myp, f, i, j, k, nx, ny, nz, sy, sz);
-        hz += coeff * exch_sum(mzp, f, i, j, k, nx, ny, nz, sy, sz);
-        hx += kan * mx;
-        hx += ax;
-        hy += ay;
-        hz += az;
-        if constexpr (MODE == 1) {
-            out[f] = hx;
-            out[n + f] = hy;
-            out[2 * n + f] = hz;
-        } else {
-            const T tx = my * hz - mz * hy;
-            const T ty = mz * hx - mx * hz;
-            const T tz = mx * hy - my * hx;
-            const T dx = p1 * tx + p2 * (my * tz - mz * ty);
-            const T dy = p1 * ty + p2 * (mz * tx - mx * tz);
-            const T dz = p1 * tz + p2 * (mx * ty - my * tx);
-            tmax = double(tx) * tx + double(ty) * ty + double(tz) * tz;
-            T nxv = mx + dx, nyv = my + dy, nzv = mz + dz;
-            const T mag = sqrt(nxv * nxv + nyv * nyv + nzv * nzv);
-            if (mag == T(0)) {
-                atomicMin(&ctl->bad_key, (static_cast<unsigned long long>(cur) << 36) |
-                                             static_cast<unsigned long long>(f));
-            } else {
-                const T scale = ms / mag;
-                nxv *= scale;
-                nyv *= scale;
-                nzv *= scale;
+
+    for (int k = 0; k < nz; ++k) {
+        __syncthreads();
+        const long long pk = k * sz;
+        for (int e = lt; e < 3 * TH * TW; e += kLlgThreads) {
+            const int c = e / (TH * TW), rem = e - c * (TH * TW);
+            const int yy = rem / TW, xx = rem - yy * TW;
+            const int ii = i0 - 1 + xx, jj = j0 - 1 + yy;
+            tile[c][yy][xx] = (ii >= 0 && ii < nx && jj >= 0 && jj < ny)
+                                  ? __ldg(m + c * n + pk + static_cast<long long>(jj) * nx + ii)
+                                  : T(0);
+        }
+        if (k + 1 < nz && live) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) nxt[c] = __ldg(m + c * n + pk + sz + oxy);
+        }
+        __syncthreads();
+        if (live) {
+            const long long f = pk + oxy;
+            T h[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const T center = cur[c];
+                T sum = T(0);
+                if (i > 0) sum += tile[c][ty + 1][tx] - center;
+                if (i + 1 < nx) sum += tile[c][ty + 1][tx + 2] - center;
+                if (j > 0) sum += tile[c][ty][tx + 1] - center;
+                if (j + 1 < ny) sum += tile[c][ty + 2][tx + 1] - center;
+                if (k > 0) sum += prv[c] - center;
+                if (k + 1 < nz) sum += nxt[c] - center;
+                h[c] = __ldg(hd + c * n + f) + coeff * sum;
             }
-            out[f] = nxv;
-            out[n + f] = nyv;
-            out[2 * n + f] = nzv;
+            const T mx = cur[0], my = cur[1], mz = cur[2];
+            T hx = h[0], hy = h[1], hz = h[2];
+            hx += kan * mx;
+            hx += ax;
+            hy += ay;
+            hz += az;
+            if constexpr (MODE == 1) {
+                out[f] = hx;
+                out[n + f] = hy;
+                out[2 * n + f] = hz;
+            } else {
+                const T tqx = my * hz - mz * hy;
+                const T tqy = mz * hx - mx * hz;
+                const T tqz = mx * hy - my * hx;
+                const T dx = p1 * tqx + p2 * (my * tqz - mz * tqy);
+                const T dy = p1 * tqy + p2 * (mz * tqx - mx * tqz);
+                const T dz = p1 * tqz + p2 * (mx * tqy - my * tqx);
+                tmax = fmax(tmax, double(tqx) * tqx + double(tqy) * tqy + double(tqz) * tqz);
+                T nxv = mx + dx, nyv = my + dy, nzv = mz + dz;
+                const T mag = sqrt(nxv * nxv + nyv * nyv + nzv * nzv);
+                if (mag == T(0)) {
+                    atomicMin(&ctl->bad_key, (static_cast<unsigned long long>(cur_step) << 36) |
+                                                 static_cast<unsigned long long>(f));
+                } else {
+                    const T scale = ms / mag;
+                    nxv *= scale;
+                    nyv *= scale;
+                    nzv *= scale;
+                }
+                out[f] = nxv;
+                out[n + f] = nyv;
+                out[2 * n + f] = nzv;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            prv[c] = cur[c];
+            cur[c] = nxt[c];
         }
     }
     if constexpr (MODE == 0) {
         __shared__ double red[kLlgThreads / 32];
         tmax = warp_max(tmax);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = tmax;
+        if ((lt & 31) == 0) red[lt >> 5] = tmax;
         __syncthreads();
-        if (threadIdx.x < 32) {
-            double v = threadIdx.x < kLlgThreads / 32 ? red[threadIdx.x] : 0.0;
+        if (lt < 32) {
+            double v = lt < kLlgThreads / 32 ? red[lt] : 0.0;
             v = warp_max(v);
-            if (threadIdx.x == 0) atomicMax(&ctl->torque_sq_bits, __double_as_longlong(v));
+            if (lt == 0) tpart[blockIdx.y * gridDim.x + blockIdx.x] = v;
         }
+    }
+}
+
+// max over the per-CTA torque partials -> ctl->torque_sq_bits
+__global__ void k_torque_partials(const double* __restrict__ tpart, int nb, StepCtl* ctl) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) v = fmax(v, tpart[b]);
+    __shared__ double red[8];
+    v = warp_max(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+        ctl->torque_sq_bits = static_cast<unsigned long long>(__double_as_longlong(t));
     }
 }
 
@@ -277,13 +333,23 @@ int reduce_blocks(long long n) {
     return static_cast<int>(b < kRedBlocks ? (b < 1 ? 1 : b) : kRedBlocks);
 }
 
+int llg_blocks(const Geom& g) {
+    return ((g.nx + kTileX - 1) / kTileX) * ((g.ny + kTileY - 1) / kTileY);
+}
+
+void launch_torque_partials(const double* tpart, int nb, StepCtl* ctl, cudaStream_t stream) {
+    k_torque_partials<<<1, 256, 0, stream>>>(tpart, nb, ctl);
+    check_launch();
+}
+
 template <typename T>
 void launch_llg(int mode, const T* m, const T* hd, T* out, const Geom& g, double exch_coeff,
-                double aniso_coeff, StepCtl* ctl, cudaStream_t stream) {
-    const unsigned blocks = static_cast<unsigned>((g.n + kLlgThreads - 1) / kLlgThreads);
+                double aniso_coeff, StepCtl* ctl, double* tpart, cudaStream_t stream) {
+    const dim3 grid((g.nx + kTileX - 1) / kTileX, (g.ny + kTileY - 1) / kTileY);
+    const dim3 block(kTileX, kTileY);
     const T coeff = static_cast<T>(exch_coeff), kan = static_cast<T>(aniso_coeff);
-    if (mode == 0) k_llg<T, 0><<<blocks, kLlgThreads, 0, stream>>>(m, hd, out, g, coeff, kan, ctl);
-    else k_llg<T, 1><<<blocks, kLlgThreads, 0, stream>>>(m, hd, out, g, coeff, kan, ctl);
+    if (mode == 0) k_llg<T, 0><<<grid, block, 0, stream>>>(m, hd, out, g, coeff, kan, ctl, tpart);
+    else k_llg<T, 1><<<grid, block, 0, stream>>>(m, hd, out, g, coeff, kan, ctl, tpart);
     check_launch();
 }
 
@@ -320,7 +386,7 @@ void launch_tensor_octant(double* E, int nx, int ny, int nz, double delta, cudaS
 
 #define MMB_INST(T)                                                                                 \
     template void launch_llg<T>(int, const T*, const T*, T*, const Geom&, double, double, StepCtl*, \
-                                cudaStream_t);                                                     \
+                                double*, cudaStream_t);                                            \
     template void launch_sum3<T>(const T*, long long, double*, double*, cudaStream_t);              \
     template void launch_torque_max<T>(const T*, const T*, long long, unsigned long long*,          \
                                        cudaStream_t);                                              \

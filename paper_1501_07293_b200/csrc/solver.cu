@@ -132,12 +132,14 @@ public:
         m_[1].alloc(3 * n);
         hd_.alloc(3 * n);
         heff_.alloc(3 * n);
-        S_.alloc(static_cast<size_t>(3) * g.nz * g.ly * (fast_ ? g.xh : g.xp));
+        S_.alloc(fast_ ? static_cast<size_t>(3) * g.nz * g.ny * g.xh
+                      : static_cast<size_t>(3) * g.nz * g.ly * g.xp);
         kspec_.alloc(static_cast<size_t>(6) * g.zh * g.yh * g.xh);
         twx_.alloc(g.lx);
         twy_.alloc(g.ly);
         twz_.alloc(g.lz);
         partial_.alloc(3 * 1024);
+        tpart_.alloc(llg_blocks(g));
         red_.alloc(8);
         ctl_.alloc(1);
         ck(cudaMallocHost(&ctl_host_, sizeof(StepCtl)), "cudaMallocHost");
@@ -255,6 +257,7 @@ public:
     }
 
     double last_torque_sq() override {
+        launch_torque_partials(tpart_.p, llg_blocks(g_), ctl_.p, stream_);
         fetch_ctl();
         double v;
         std::memcpy(&v, &ctl_host_->torque_sq_bits, sizeof(v));
@@ -373,7 +376,7 @@ public:
     size_t device_bytes() const override {
         return m_[0].bytes() + m_[1].bytes() + hd_.bytes() + heff_.bytes() + S_.bytes() +
                kspec_.bytes() + twx_.bytes() + twy_.bytes() + twz_.bytes() + partial_.bytes() +
-               red_.bytes() + ctl_.bytes();
+               red_.bytes() + tpart_.bytes() + ctl_.bytes();
     }
 
 private:
@@ -471,13 +474,13 @@ private:
 
     void enqueue_step_eager(int cur, cudaEvent_t* ev = nullptr) {
         enqueue_demag(m_[cur].p, hd_.p, 1, ev);
-        launch_llg<T>(0, m_[cur].p, hd_.p, m_[cur ^ 1].p, g_, exch_coeff_, aniso_coeff_, ctl_.p, stream_);
+        launch_llg<T>(0, m_[cur].p, hd_.p, m_[cur ^ 1].p, g_, exch_coeff_, aniso_coeff_, ctl_.p, tpart_.p, stream_);
         if (ev) ck(cudaEventRecord(ev[kernel_names().size()], stream_), "record");
     }
 
     void enqueue_heff() {
         enqueue_demag(m_[cur_].p, hd_.p, 2);
-        launch_llg<T>(1, m_[cur_].p, hd_.p, heff_.p, g_, exch_coeff_, aniso_coeff_, ctl_.p, stream_);
+        launch_llg<T>(1, m_[cur_].p, hd_.p, heff_.p, g_, exch_coeff_, aniso_coeff_, ctl_.p, tpart_.p, stream_);
     }
 
     void ensure_graph(int cur) {
@@ -530,7 +533,7 @@ private:
     DevBuf<T> m_[2], hd_, heff_;
     DevBuf<cx<T>> S_, twx_, twy_, twz_;
     DevBuf<T> kspec_;
-    DevBuf<double> partial_, red_;
+    DevBuf<double> partial_, red_, tpart_;
     DevBuf<StepCtl> ctl_;
     StepCtl* ctl_host_ = nullptr;
     cudaGraphExec_t graph_[2] = {nullptr, nullptr};
