@@ -53,6 +53,19 @@ __device__ __forceinline__ long long sf_row(int kx, int c, int z, int nz, int ny
     return ((static_cast<long long>(kx) * 3 + c) * nz + z) * ny;
 }
 
+// Ampere-style async global->shared copy of one element (LDGSTS), bypassing registers.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // Stage-A twiddles W_L^{n1*k2} staged in shared memory as [k2][n1] (unit stride across the
 // n1-consecutive lanes of stage A: bank-conflict free, no global loads on the hot path).
 template <typename T, int LOG2L>
@@ -157,12 +170,15 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
     const int tid = threadIdx.x;
     stage_twiddles<T, LOG2L>(tws, tw);
 
-    // stage the 2P half-spectrum rows: task (k, r), r fastest (coalesced reads)
+    // stage the 2P half-spectrum rows with async copies (all loads in flight at once):
+    // task (k, r), r fastest (coalesced reads)
     for (int it = tid; it < XH * 2 * P; it += blockDim.x) {
         const int r = it % (2 * P), k = it / (2 * P);
         const int y = y0 + r;
-        sm[r * RP + k] = (y < ny) ? S[sf_row(k, c, z, nz, ny) + y] : cx<T>{0, 0};
+        if (y < ny) cp_async<sizeof(cx<T>)>(sm + r * RP + k, S + sf_row(k, c, z, nz, ny) + y);
+        else sm[r * RP + k] = cx<T>{0, 0};
     }
+    cp_async_wait_all();
     __syncthreads();
     // stage A on Z = A + iB (full circle from the two Hermitian halves)
     cx<T> v[N2];

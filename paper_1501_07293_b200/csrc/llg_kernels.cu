@@ -47,10 +47,10 @@ __device__ __forceinline__ T exch_sum(const T* __restrict__ src, long long f, in
     return sum;
 }
 
-// K6: fused local terms + Euler + renormalisation, 2.5-D blocked: each CTA owns a 32 x 8
-// (x, y) column and marches through z; the current plane's tile (+1-cell halo) of M is
-// staged in shared memory for the x/y neighbours, the z neighbours ride in registers. M and
-// H_demag are read once and M_{t+1} written once (ping-pong buffers).
+// K6: fused local terms + Euler + renormalisation, one thread per cell, 32 x 8 (x, y) tiles
+// per CTA and one z plane per grid row (no integer division; x/y neighbours of a tile hit
+// L1, z neighbours L2). M and H_demag are read once from HBM, M_{t+1} written once
+// (ping-pong buffers).
 //   H = H_demag; H += coeff * exch_sum (local_fields.cpp:39; neighbour order -x,+x,-y,+y,
 //   -z,+z with Neumann skips, :27-38); Hx += (hk/ms) Mx (local_fields.hpp:28-31);
 //   H += applied (local_fields.hpp:43-55)
@@ -58,103 +58,79 @@ __device__ __forceinline__ T exch_sum(const T* __restrict__ src, long long f, in
 //   mag = sqrt(Mx^2 + My^2 + Mz^2); M *= T(ms)/mag (vector_field.hpp:56-76)
 // MODE 1 writes H_eff instead (field assembly only). Per-CTA torque maxima go to tpart[]
 // (reduced on demand), so the hot path has no same-address atomics.
+template <typename T>
+__device__ __forceinline__ T exch1(const T* __restrict__ p, int i, int j, int k, int nx, int ny,
+                                   int nz, int sy, int sz) {
+    const T center = __ldg(p);
+    T sum = T(0);
+    if (i > 0) sum += __ldg(p - 1) - center;
+    if (i + 1 < nx) sum += __ldg(p + 1) - center;
+    if (j > 0) sum += __ldg(p - sy) - center;
+    if (j + 1 < ny) sum += __ldg(p + sy) - center;
+    if (k > 0) sum += __ldg(p - sz) - center;
+    if (k + 1 < nz) sum += __ldg(p + sz) - center;
+    return sum;
+}
+
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kLlgThreads) k_llg(const T* __restrict__ m, const T* __restrict__ hd,
                                                      T* __restrict__ out, Geom g, T coeff, T kan,
                                                      StepCtl* ctl, double* __restrict__ tpart) {
-    constexpr int TW = kTileX + 2, TH = kTileY + 2;
-    __shared__ T tile[3][TH][TW];
-    const long long n = g.n;
+    const int n = static_cast<int>(g.n);
     const int nx = g.nx, ny = g.ny, nz = g.nz;
-    const long long sz = static_cast<long long>(nx) * ny;
-    const T ax = static_cast<T>(ctl->field[0]);
-    const T ay = static_cast<T>(ctl->field[1]);
-    const T az = static_cast<T>(ctl->field[2]);
-    const T p1 = static_cast<T>(ctl->p1);
-    const T p2 = static_cast<T>(ctl->p2);
-    const T ms = static_cast<T>(ctl->ms);
-    const long long cur_step = ctl->cur_step;
+    const int sy = nx, sz = nx * ny;
     const int tx = threadIdx.x, ty = threadIdx.y, lt = ty * kTileX + tx;
-    if (MODE == 0 && blockIdx.x == 0 && blockIdx.y == 0 && lt == 0) ctl->step = cur_step + 1;
-
-    const int i0 = blockIdx.x * kTileX, j0 = blockIdx.y * kTileY;
-    const int i = i0 + tx, j = j0 + ty;
-    const bool live = i < nx && j < ny;
-    const long long oxy = static_cast<long long>(j) * nx + i;
-    T prv[3] = {T(0), T(0), T(0)}, cur[3], nxt[3] = {T(0), T(0), T(0)};
-#pragma unroll
-    for (int c = 0; c < 3; ++c) cur[c] = live ? __ldg(m + c * n + oxy) : T(0);
+    const long long cur_step = ctl->cur_step;
+    if (MODE == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lt == 0)
+        ctl->step = cur_step + 1;
+    const int i = blockIdx.x * kTileX + tx, j = blockIdx.y * kTileY + ty, k = blockIdx.z;
     double tmax = 0.0;
-
-    for (int k = 0; k < nz; ++k) {
-        __syncthreads();
-        const long long pk = k * sz;
-        for (int e = lt; e < 3 * TH * TW; e += kLlgThreads) {
-            const int c = e / (TH * TW), rem = e - c * (TH * TW);
-            const int yy = rem / TW, xx = rem - yy * TW;
-            const int ii = i0 - 1 + xx, jj = j0 - 1 + yy;
-            tile[c][yy][xx] = (ii >= 0 && ii < nx && jj >= 0 && jj < ny)
-                                  ? __ldg(m + c * n + pk + static_cast<long long>(jj) * nx + ii)
-                                  : T(0);
-        }
-        if (k + 1 < nz && live) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) nxt[c] = __ldg(m + c * n + pk + sz + oxy);
-        }
-        __syncthreads();
-        if (live) {
-            const long long f = pk + oxy;
-            T h[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const T center = cur[c];
-                T sum = T(0);
-                if (i > 0) sum += tile[c][ty + 1][tx] - center;
-                if (i + 1 < nx) sum += tile[c][ty + 1][tx + 2] - center;
-                if (j > 0) sum += tile[c][ty][tx + 1] - center;
-                if (j + 1 < ny) sum += tile[c][ty + 2][tx + 1] - center;
-                if (k > 0) sum += prv[c] - center;
-                if (k + 1 < nz) sum += nxt[c] - center;
-                h[c] = __ldg(hd + c * n + f) + coeff * sum;
-            }
-            const T mx = cur[0], my = cur[1], mz = cur[2];
-            T hx = h[0], hy = h[1], hz = h[2];
-            hx += kan * mx;
-            hx += ax;
-            hy += ay;
-            hz += az;
-            if constexpr (MODE == 1) {
-                out[f] = hx;
-                out[n + f] = hy;
-                out[2 * n + f] = hz;
+    if (i < nx && j < ny) {
+        const T ax = static_cast<T>(ctl->field[0]);
+        const T ay = static_cast<T>(ctl->field[1]);
+        const T az = static_cast<T>(ctl->field[2]);
+        const int f = k * sz + j * sy + i;
+        const T* px = m + f;
+        const T* py = px + n;
+        const T* pz = py + n;
+        const T mx = __ldg(px), my = __ldg(py), mz = __ldg(pz);
+        T hx = __ldg(hd + f), hy = __ldg(hd + n + f), hz = __ldg(hd + 2 * n + f);
+        hx += coeff * exch1(px, i, j, k, nx, ny, nz, sy, sz);
+        hy += coeff * exch1(py, i, j, k, nx, ny, nz, sy, sz);
+        hz += coeff * exch1(pz, i, j, k, nx, ny, nz, sy, sz);
+        hx += kan * mx;
+        hx += ax;
+        hy += ay;
+        hz += az;
+        if constexpr (MODE == 1) {
+            out[f] = hx;
+            out[n + f] = hy;
+            out[2 * n + f] = hz;
+        } else {
+            const T p1 = static_cast<T>(ctl->p1);
+            const T p2 = static_cast<T>(ctl->p2);
+            const T ms = static_cast<T>(ctl->ms);
+            const T tqx = my * hz - mz * hy;
+            const T tqy = mz * hx - mx * hz;
+            const T tqz = mx * hy - my * hx;
+            const T dx = p1 * tqx + p2 * (my * tqz - mz * tqy);
+            const T dy = p1 * tqy + p2 * (mz * tqx - mx * tqz);
+            const T dz = p1 * tqz + p2 * (mx * tqy - my * tqx);
+            tmax = double(tqx) * tqx + double(tqy) * tqy + double(tqz) * tqz;
+            T nxv = mx + dx, nyv = my + dy, nzv = mz + dz;
+            const T mag = sqrt(nxv * nxv + nyv * nyv + nzv * nzv);
+            if (mag == T(0)) {
+                atomicMin(&ctl->bad_key, (static_cast<unsigned long long>(cur_step) << 36) |
+                                             static_cast<unsigned long long>(f));
             } else {
-                const T tqx = my * hz - mz * hy;
-                const T tqy = mz * hx - mx * hz;
-                const T tqz = mx * hy - my * hx;
-                const T dx = p1 * tqx + p2 * (my * tqz - mz * tqy);
-                const T dy = p1 * tqy + p2 * (mz * tqx - mx * tqz);
-                const T dz = p1 * tqz + p2 * (mx * tqy - my * tqx);
-                tmax = fmax(tmax, double(tqx) * tqx + double(tqy) * tqy + double(tqz) * tqz);
-                T nxv = mx + dx, nyv = my + dy, nzv = mz + dz;
-                const T mag = sqrt(nxv * nxv + nyv * nyv + nzv * nzv);
-                if (mag == T(0)) {
-                    atomicMin(&ctl->bad_key, (static_cast<unsigned long long>(cur_step) << 36) |
-                                                 static_cast<unsigned long long>(f));
-                } else {
-                    const T scale = ms / mag;
-                    nxv *= scale;
-                    nyv *= scale;
-                    nzv *= scale;
-                }
-                out[f] = nxv;
-                out[n + f] = nyv;
-                out[2 * n + f] = nzv;
+                const T scale = ms / mag;
+                nxv *= scale;
+                nyv *= scale;
+                nzv *= scale;
             }
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            prv[c] = cur[c];
-            cur[c] = nxt[c];
+            out[f] = nxv;
+            out[n + f] = nyv;
+            out[2 * n + f] = nzv;
         }
     }
     if constexpr (MODE == 0) {
@@ -165,7 +141,7 @@ __global__ void __launch_bounds__(kLlgThreads) k_llg(const T* __restrict__ m, co
         if (lt < 32) {
             double v = lt < kLlgThreads / 32 ? red[lt] : 0.0;
             v = warp_max(v);
-            if (lt == 0) tpart[blockIdx.y * gridDim.x + blockIdx.x] = v;
+            if (lt == 0) tpart[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = v;
         }
     }
 }
@@ -334,7 +310,7 @@ int reduce_blocks(long long n) {
 }
 
 int llg_blocks(const Geom& g) {
-    return ((g.nx + kTileX - 1) / kTileX) * ((g.ny + kTileY - 1) / kTileY);
+    return ((g.nx + kTileX - 1) / kTileX) * ((g.ny + kTileY - 1) / kTileY) * g.nz;
 }
 
 void launch_torque_partials(const double* tpart, int nb, StepCtl* ctl, cudaStream_t stream) {
@@ -345,7 +321,7 @@ void launch_torque_partials(const double* tpart, int nb, StepCtl* ctl, cudaStrea
 template <typename T>
 void launch_llg(int mode, const T* m, const T* hd, T* out, const Geom& g, double exch_coeff,
                 double aniso_coeff, StepCtl* ctl, double* tpart, cudaStream_t stream) {
-    const dim3 grid((g.nx + kTileX - 1) / kTileX, (g.ny + kTileY - 1) / kTileY);
+    const dim3 grid((g.nx + kTileX - 1) / kTileX, (g.ny + kTileY - 1) / kTileY, g.nz);
     const dim3 block(kTileX, kTileY);
     const T coeff = static_cast<T>(exch_coeff), kan = static_cast<T>(aniso_coeff);
     if (mode == 0) k_llg<T, 0><<<grid, block, 0, stream>>>(m, hd, out, g, coeff, kan, ctl, tpart);

@@ -122,6 +122,8 @@ public:
         g.yh = g.ly == 1 ? 1 : g.ly / 2 + 1;
         g.zh = g.lz == 1 ? 1 : g.lz / 2 + 1;
         g.n = static_cast<long long>(d.nx) * d.ny * d.nz;
+        if (3 * g.n >= (1LL << 31))
+            throw std::invalid_argument("mmb: more than 715M cells per device (32-bit cell indexing)");
         g.rows = static_cast<long long>(d.ny) * d.nz;
 
         const char* force_general = std::getenv("MMB_GENERAL_PATH");
