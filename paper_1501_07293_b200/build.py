@@ -74,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         results = list(ex.map(lambda u: _compile(u, force, verbose), UNITS))
     objs = [o for o, _ in results]
     if force or any(changed for _, changed in results) or not os.path.exists(LIB):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+        cmd = [NVCC] + ARCH + ["-shared", "-Xlinker", "-soname=libmmb.so", "-o", LIB] + objs + ["-lcudart"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -75,3 +75,36 @@ def test_host_spec_validation():
     assert ramp.value_at(ramp.end)[0] == 0.0
     assert standard_problem_3_benchmark(8).material.hk == 100.0
     assert abs(MaterialParams(1.3e7, 800.0).exchange_coefficient(1.0) - 32.33) <= 0.01
+
+
+ADAPTER_BIN = os.path.join(ROOT, "build", "adapter_check")
+
+
+def _build_adapter():
+    import subprocess
+    if not os.path.exists("/root/reference/proj/include"):
+        return os.path.exists(ADAPTER_BIN)
+    from oracle import ref
+    if not ref.available():
+        ref.build()
+    os.makedirs(os.path.dirname(ADAPTER_BIN), exist_ok=True)
+    cmd = ["/usr/bin/g++", "-std=c++20", "-O1", "-I/root/reference/proj/include",
+           f"-I{ROOT}/include", f"-I{ROOT}/integration", f"{ROOT}/integration/adapter_check.cpp",
+           "-o", ADAPTER_BIN, _lib.LIB_PATH, ref.LIB_PATH,
+           f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}", f"-Wl,-rpath,{os.path.dirname(ref.LIB_PATH)}",
+           "-Wl,-rpath,$ORIGIN/../paper_1501_07293_b200", "-Wl,-rpath,$ORIGIN/../oracle/_ref"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return True
+
+
+def test_reference_side_adapter_compiles_and_fails_loudly_without_gpu():
+    """integration/b200_simulation.hpp (the mmsim::SimulationBase binding documented in
+    INTEGRATION.md) compiles against the reference headers and links libmmb.so."""
+    import subprocess
+    import torch
+    if not _build_adapter():
+        pytest.skip("reference headers unavailable and no prebuilt adapter")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by the gpu test")
+    r = subprocess.run([ADAPTER_BIN], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2 and "no CUDA device" in r.stdout

@@ -276,3 +276,14 @@ def test_512x512x8_f32_properties(path):
     g = O.Grid(512, 512, 8, 1.0)
     want = O.demag_field_fft(m1.astype(np.float64), g)
     assert rel(sim.demag_field(m1), want) <= 1e-5
+
+
+def test_reference_side_adapter_runs():
+    """The SimulationBase adapter (integration/b200_simulation.hpp), prebuilt here by the CPU
+    suite, drives the B200 path through the C-ABI: 10 steps, 2 cadence records."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(HERE), "build", "adapter_check")
+    if not os.path.exists(exe):
+        pytest.skip("adapter binary not built (CPU suite builds it where /root/reference exists)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -1,0 +1,115 @@
+"""Multi-rank host path on CPU: world_size-2 (and 3) gloo runs of the slab-decomposed demag
+convolution (paper_1501_07293_b200/shard.py: partition, forward/backward all-to-all transpose,
+halo exchange) with NumPy FFTs standing in for the per-rank kernels; the gathered field must
+equal the single-process oracle (the reference's DemagSolver restated) to FFT round-off."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import mmsim_oracle as O
+from paper_1501_07293_b200 import shard
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _wrapped_tensor_spectrum(g, lx, ly, lz):
+    oz = np.arange(-(g.nz - 1), g.nz)
+    oy = np.arange(-(g.ny - 1), g.ny)
+    ox = np.arange(-(g.nx - 1), g.nx)
+    K, J, I = np.meshgrid(oz, oy, ox, indexing="ij")
+    comps = O.tensor_entry(I, J, K, g.delta)
+    out = []
+    for c in range(6):
+        t = np.zeros((lz, ly, lx))
+        t[K % lz, J % ly, I % lx] = comps[c]
+        out.append(np.fft.rfftn(t))
+    return np.stack(out)  # [6, lz, ly, xh]
+
+
+def _rank_main(rank, world, port, nx, ny, nz, delta, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = O.Grid(nx, ny, nz, delta)
+        p = shard.plan(nx, ny, nz, world)
+        assert p.axis == "z"
+        lx, ly, lz = shard.padded_len(nx), shard.padded_len(ny), shard.padded_len(nz)
+        rng = np.random.default_rng(7)
+        m = rng.uniform(-800, 800, (3, nz, ny, nx))
+        z0, z1 = p.slab(rank)
+        m_slab = m[:, z0:z1]
+        # KX stand-in: r2c along x on the local rows, kx-major [Xh, 3, nslab, ny]
+        s_local = np.fft.rfft(m_slab, n=lx, axis=-1).transpose(3, 0, 1, 2).copy()
+        cols = shard.transpose_forward(p, rank, torch.from_numpy(s_local)).numpy()
+        k0, k1 = p.cols[rank]
+        spec = _wrapped_tensor_spectrum(g, lx, ly, lz)[:, :, :, k0:k1]  # [6, lz, ly, ncols]
+        # KYZ stand-in: y/z FFTs of the live planes, MAC, inverse, crop
+        a = np.fft.fftn(cols, s=(lz, ly), axes=(2, 3))  # [ncols, 3, lz, ly]
+        kk = spec.transpose(0, 3, 1, 2)                   # [6, ncols, lz, ly]
+        rows = ((0, 1, 2), (1, 3, 4), (2, 4, 5))
+        h = np.stack([sum(kk[rows[c][j]] * a[:, j] for j in range(3)) for c in range(3)], axis=1)
+        h = np.fft.ifftn(h, axes=(2, 3))[:, :, :nz, :ny]
+        back = shard.transpose_backward(p, rank, torch.from_numpy(np.ascontiguousarray(h))).numpy()
+        # KXI stand-in
+        h_slab = np.fft.irfft(back.transpose(1, 2, 3, 0), n=lx, axis=-1)[..., :nx]
+        # halo exchange of M
+        below, above = shard.halo_exchange(p, rank, torch.from_numpy(np.ascontiguousarray(m_slab)))
+        ok_halo = True
+        if below is not None:
+            ok_halo &= np.array_equal(below.numpy(), m[:, z0 - 1])
+        if above is not None:
+            ok_halo &= np.array_equal(above.numpy(), m[:, z1])
+        full = [torch.zeros(1) for _ in range(world)]
+        dist.all_gather_object(full, (z0, z1, h_slab, ok_halo))
+        if rank == 0:
+            hh = np.zeros((3, nz, ny, nx))
+            halos = True
+            for a_, b_, hs, okh in full:
+                hh[:, a_:b_] = hs
+                halos &= okh
+            want = O.demag_field_fft(m, g)
+            q.put((O.max_relative_error(hh, want), halos, p.bytes_per_step(4)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape", [(2, (12, 10, 6)), (3, (9, 7, 7)), (2, (16, 8, 2))])
+def test_sharded_demag_equals_single_process(world, shape):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, *shape, 2.0, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    err, halos, nbytes = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert err <= 1e-12
+    assert halos
+    assert nbytes["transposes"] > 0
+
+
+def test_plan_partitions_and_counts():
+    p = shard.plan(2048, 2048, 64, 8)
+    assert p.axis == "z" and [b - a for a, b in p.slabs] == [8] * 8
+    assert sum(p.ncols(r) for r in range(8)) == 2049
+    for r in range(8):
+        assert sum(p.send_counts_forward(r)) == p.xh * 3 * p.nslab(r) * 2048
+        assert sum(p.recv_counts_forward(r)) == p.ncols(r) * 3 * 64 * 2048
+    # nz < P falls back to y-slabs
+    assert shard.plan(64, 64, 2, 4).axis == "y"
+    b = p.bytes_per_step(4)
+    # f32: each rank ships 7/8 of its 1/8 share of the 6.4 GB half spectrum each way
+    assert abs(b["transpose_each_way"] - 2049 * 3 * 8 * 2048 * 8 * 7 / 8) < 2049 * 3 * 8 * 2048 * 8
