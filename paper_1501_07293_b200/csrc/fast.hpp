@@ -1,7 +1,7 @@
 // fast.hpp — launchers of the fast demag path (fast_kernels.cu). Supported when
 // fast_supported<T>(g): 2 <= Lx, Ly <= 4096 (2048 for f64), nz == 1 or (2 <= nz <= 8 with
 // Lz = 16, f32), and one kx block of the spectrum fits in shared memory.
-// Spectrum scratch layout: S[kx][c][z][y], y fastest, Ly rows; tensor: [kx][c][kz][ky].
+// Spectrum scratch layout: S[kx][c][z][y], y fastest, ny rows; tensor: [kx][kz][ky][c].
 #pragma once
 
 #include <cuda_runtime.h>
@@ -20,7 +20,7 @@ template <typename T>
 void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, cudaStream_t stream);
 template <typename T>
 void launch_fast_xi(const cx<T>* S, T* h, const Geom& g, const cx<T>* tw, cudaStream_t stream);
-// Tensor spectrum [6][zh][yh][xh] (fp64) -> fast layout [xh][6][zh][yh] in T, with the
+// Tensor spectrum [6][zh][yh][xh] (fp64) -> fast layout [xh][zh][yh][6] in T, with the
 // off-diagonal sign and the 1/P scale (see launch_tensor_finalize).
 template <typename T>
 void launch_tensor_finalize_fast(const double* spec, T* out, int xh, int yh, int zh, double scale,

@@ -66,6 +66,48 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// ---- TMA (cp.async.bulk) global -> shared with an mbarrier transaction count
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// six tensor coefficients stored contiguously ([..][6]): three 2-vector loads
+template <typename T>
+__device__ __forceinline__ void load6(const T* __restrict__ p, T (&k)[6]) {
+    const cx<T>* q = reinterpret_cast<const cx<T>*>(p);
+    const cx<T> a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+    k[0] = a.x;
+    k[1] = a.y;
+    k[2] = b.x;
+    k[3] = b.y;
+    k[4] = c.x;
+    k[5] = c.y;
+}
+
 // Stage-A twiddles W_L^{n1*k2} staged in shared memory as [k2][n1] (unit stride across the
 // n1-consecutive lanes of stage A: bank-conflict free, no global loads on the hot path).
 template <typename T, int LOG2L>
@@ -261,13 +303,29 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
 
     const int nz = g.nz, ny = g.ny, xh = g.xh;
     cx<T>* tws = sm + kxb * 3 * nz * RP;
-    stage_twiddles<T, LOG2L>(tws, tw);
-    __syncthreads();
+    __shared__ __align__(8) unsigned long long bar;
     const int kx0 = blockIdx.x * kxb;
     const int kxn = min(kxb, xh - kx0);
     const int rows = kxn * 3 * nz;
     const int tid = threadIdx.x;
     cx<T>* gblk = S + sf_row(kx0, 0, 0, nz, ny); // rows of this CTA are contiguous in S
+    // TMA bulk copies of all live input rows (ny values each) into the first ny slots of
+    // their shared-memory rows, in flight together while the twiddles are staged.
+    const unsigned rowbytes = static_cast<unsigned>(ny * sizeof(cx<T>));
+    const bool bulk = (rowbytes % 16) == 0;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        if (bulk) {
+            mbar_expect_tx(&bar, rowbytes * rows);
+            for (int r = 0; r < rows; ++r) bulk_g2s(sm + r * RP, gblk + static_cast<long long>(r) * ny, rowbytes, &bar);
+        }
+    }
+    stage_twiddles<T, LOG2L>(tws, tw);
+    if (!bulk) {
+        for (int e = tid; e < rows * ny; e += NT) sm[(e / ny) * RP + e % ny] = gblk[e];
+    }
+    __syncthreads();
+    if (bulk) mbar_wait(&bar, 0);
 
     // ---- y forward, batches of RB rows
     for (int rb0 = 0; rb0 < rows; rb0 += RB) {
@@ -276,7 +334,7 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
         const int ra = rb0 + tid / N1, n1 = tid % N1;
         const bool a_task = tid < nb * N1;
         if (a_task) {
-            const cx<T>* src = gblk + static_cast<long long>(ra) * ny;
+            const cx<T>* src = sm + ra * RP;
             constexpr int NZ = L == 1 ? 1 : N2 / 2;
 #pragma unroll
             for (int n2 = 0; n2 < NZ; ++n2) {
@@ -284,6 +342,9 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
                 v[n2] = y < ny ? src[y] : cx<T>{0, 0};
             }
             DftP<N2, -1, NZ, N2>::run(v);
+        }
+        __syncthreads(); // the staged input rows are overwritten in place below
+        if (a_task) {
             cx<T>* dst = sm + ra * RP;
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) {
@@ -319,14 +380,13 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
             const int kx = kx0 + kxl;
             const bool fy = 2 * ky > ly;
             const int kyo = fy ? ly - ky : ky;
-            const T* kb = kt + static_cast<long long>(kx) * 6 * zh * yh + kyo;
+            const T* kb = kt + (static_cast<long long>(kx) * zh * yh + kyo) * 6;
             cx<T>* base = sm + (kxl * 3 * nz) * RP + fpad<LOG2L>(ky);
             if constexpr (ZM == 0) {
                 // nz == 1: MAC only
                 cx<T> a = base[0], b = base[RP], cc = base[2 * RP];
                 T k6[6];
-#pragma unroll
-                for (int q = 0; q < 6; ++q) k6[q] = __ldg(kb + q * yh);
+                load6<T>(kb, k6);
                 if (fy) {
                     k6[1] = -k6[1];
                     k6[4] = -k6[4];
@@ -348,8 +408,7 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
 #pragma unroll
                 for (int kzo = 0; kzo <= 8; ++kzo) {
                     T k6[6];
-#pragma unroll
-                    for (int q = 0; q < 6; ++q) k6[q] = __ldg(kb + (q * zh + kzo) * yh);
+                    load6<T>(kb + kzo * yh * 6, k6);
                     if (fy) {
                         k6[1] = -k6[1];
                         k6[4] = -k6[4];

@@ -86,7 +86,8 @@ __global__ void k_finalize(const double* __restrict__ spec, T* __restrict__ out,
     out[c * count + f] = static_cast<T>(sgn * scale * spec[c * count + f]);
 }
 
-// Fast-path layout [kx][c][kz][ky] (ky fastest): one contiguous tensor slab per kx.
+// Fast-path layout [kx][kz][ky][c] (the six coefficients of one frequency contiguous, ky next):
+// one contiguous tensor slab per kx, three 2-vector loads per frequency in the MAC.
 template <typename T>
 __global__ void k_finalize_fast(const double* __restrict__ spec, T* __restrict__ out, int xh, int yh,
                                 int zh, double scale) {
@@ -98,7 +99,7 @@ __global__ void k_finalize_fast(const double* __restrict__ spec, T* __restrict__
     const long long r = f / xh;
     const int ky = static_cast<int>(r % yh), kz = static_cast<int>(r / yh);
     const double sgn = (c == 1 || c == 2 || c == 4) ? -1.0 : 1.0;
-    out[((static_cast<long long>(kx) * 6 + c) * zh + kz) * yh + ky] =
+    out[((static_cast<long long>(kx) * zh + kz) * yh + ky) * 6 + c] =
         static_cast<T>(sgn * scale * spec[c * count + f]);
 }
 
