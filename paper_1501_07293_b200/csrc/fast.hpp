@@ -16,8 +16,17 @@ template <typename T> void prepare_fast_kernels(const Geom& g);
 template <typename T>
 void launch_fast_xf(const T* m, cx<T>* S, const Geom& g, const cx<T>* tw, StepCtl* ctl,
                     const StageTable& st, int prologue, cudaStream_t stream);
+// KYZ; block 0 optionally runs the step prologue (schedule, sticky alpha, prefactors).
 template <typename T>
-void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, cudaStream_t stream);
+void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, StepCtl* ctl,
+                    const StageTable& st, int prologue, cudaStream_t stream);
+// KXS: fused x-c2r -> local terms + LLG update (M -> mout) -> x-r2c of mout, S in place.
+// Writes one torque partial per CTA (fast_xstep_blocks of them) to tpart.
+template <typename T>
+void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>* tw,
+                       double exch_coeff, double aniso_coeff, StepCtl* ctl, double* tpart,
+                       cudaStream_t stream);
+template <typename T> int fast_xstep_blocks(const Geom& g);
 template <typename T>
 void launch_fast_xi(const cx<T>* S, T* h, const Geom& g, const cx<T>* tw, cudaStream_t stream);
 // Tensor spectrum [6][zh][yh][xh] (fp64) -> fast layout [xh][zh][yh][6] in T, with the

@@ -17,6 +17,7 @@
 
 #include "fast.hpp"
 #include "fft4.cuh"
+#include "llg_cell.cuh"
 
 namespace mmb {
 
@@ -292,7 +293,7 @@ constexpr int yz_threads() {
 template <typename T, int LOG2L, int ZM>
 __global__ void __launch_bounds__(yz_threads<LOG2L>())
     k_yz(cx<T>* __restrict__ S, Geom g, const cx<T>* __restrict__ tw, const T* __restrict__ kt,
-         int kxb) {
+         int kxb, StepCtl* ctl, StageTable st, int prologue) {
     using SP = Split<LOG2L>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2;
     constexpr int RP = fpitch<LOG2L>();
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
     const int nz = g.nz, ny = g.ny, xh = g.xh;
     cx<T>* tws = sm + kxb * 3 * nz * RP;
     __shared__ __align__(8) unsigned long long bar;
+    if (prologue && blockIdx.x == 0 && threadIdx.x == 0) step_prologue(ctl, st, prologue);
     const int kx0 = blockIdx.x * kxb;
     const int kxn = min(kxb, xh - kx0);
     const int rows = kxn * 3 * nz;
@@ -474,6 +476,233 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
     }
 }
 
+// ------------------------------------------------------------------ KXS: x^-1, LLG, x (fused)
+// One CTA per (TR consecutive y rows, one z plane), all three components:
+//   1. x-c2r of the convolved half spectra S -> H_demag tile (shared memory only),
+//   2. local terms + Euler + renormalisation for the TR x nx cells (CellLLG, exact
+//      reference rounding) -> M_{t+1} to HBM,
+//   3. x-r2c of the new tile -> the half spectra S for the next step, in place.
+// H_demag never reaches HBM and M_{t+1} is not re-read: per step the x side moves
+// S in + S out + M_t + M_{t+1} instead of three separate passes.
+template <int LOG2L>
+struct XS {
+    using SP = Split<LOG2L>;
+    static constexpr int P = 3 * (SP::N2 >= 128 ? 1 : 128 / SP::N2); // row pairs
+    static constexpr int TR = 2 * P / 3;                              // y rows per CTA
+    static constexpr int NT = P * SP::N2;                             // threads
+    static constexpr int XHP = ((1 << LOG2L) / 2 + 1) | 1;            // staging pitch (odd)
+    static constexpr int EX = SP::N1 + 1;
+    static constexpr int ZP = (1 << LOG2L) + 1;
+    static constexpr int A0 = 3 * TR * XHP, A1 = P * SP::N2 * EX, A2 = P * ZP;
+    static constexpr int AREA = A0 > A1 ? (A0 > A2 ? A0 : A2) : (A1 > A2 ? A1 : A2);
+};
+template <typename T, int LOG2L>
+constexpr int xs_smem_bytes() {
+    return (XS<LOG2L>::AREA + (1 << LOG2L)) * static_cast<int>(sizeof(cx<T>));
+}
+
+template <typename T, int LOG2L>
+constexpr int xs_min_blocks() {
+    // two CTAs per SM when their shared memory fits (registers capped accordingly)
+    return 2 * xs_smem_bytes<T, LOG2L>() + 4096 <= 228 * 1024 ? 2 : 1;
+}
+
+template <typename T, int LOG2L>
+__global__ void __launch_bounds__(XS<LOG2L>::NT, xs_min_blocks<T, LOG2L>())
+    k_xstep(cx<T>* __restrict__ S, const T* __restrict__ m, T* __restrict__ mout, Geom g,
+            const cx<T>* __restrict__ tw, T coeff, T kan, StepCtl* ctl, double* __restrict__ tpart) {
+    using SP = Split<LOG2L>;
+    using X = XS<LOG2L>;
+    constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = X::P, TR = X::TR, NT = X::NT;
+    constexpr int XH = L / 2 + 1, XHP = X::XHP, EX = X::EX, ZP = X::ZP;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+    T* hm = reinterpret_cast<T*>(smem_raw); // [3*TR][nx] tile: H_demag, then M_{t+1}
+    cx<T>* tws = sm + X::AREA;
+
+    const int y0 = blockIdx.x * TR, z = blockIdx.y;
+    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    const int n = static_cast<int>(g.n);
+    const int tid = threadIdx.x;
+    const long long cur_step = ctl->cur_step;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->step = cur_step + 1;
+
+    // ---- 1a. stage the 3*TR convolved half-spectrum rows (async copies)
+    for (int it = tid; it < XH * 3 * TR; it += NT) {
+        const int r = it % (3 * TR), k = it / (3 * TR);
+        const int c = r / TR, y = y0 + (r - c * TR);
+        if (y < ny) cp_async<sizeof(cx<T>)>(sm + r * XHP + k, S + sf_row(k, c, z, nz, ny) + y);
+        else sm[r * XHP + k] = cx<T>{0, 0};
+    }
+    stage_twiddles<T, LOG2L>(tws, tw);
+    cp_async_wait_all();
+    __syncthreads();
+
+    // ---- 1b. inverse stage A on Z = A + iB (rows 2p, 2p+1 of the same component)
+    cx<T> v[N2];
+    const bool a_task = tid < P * N1;
+    const int pa = tid / N1, n1 = tid % N1;
+    if (a_task) {
+        const cx<T>* A = sm + (2 * pa) * XHP;
+        const cx<T>* B = A + XHP;
+#pragma unroll
+        for (int n2 = 0; n2 < N2; ++n2) {
+            const int k = n1 + N1 * n2;
+            cx<T> zv;
+            if (k == 0 || 2 * k == L) {
+                zv = cx<T>{A[k].x, B[k].x};
+            } else if (2 * k < L) {
+                const cx<T> a = A[k], b = B[k];
+                zv = cx<T>{a.x - b.y, a.y + b.x};
+            } else {
+                const cx<T> a = A[L - k], b = B[L - k];
+                zv = cx<T>{a.x + b.y, b.x - a.y};
+            }
+            v[n2] = zv;
+        }
+        DftP<N2, +1, N2, N2>::run(v);
+    }
+    __syncthreads();
+    if (a_task) {
+        cx<T>* ex = sm + (pa * N2) * EX + n1;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+            cx<T> w = v[k2];
+            if (k2 > 0) w = cmulc(w, tws[k2 * N1 + n1]);
+            ex[k2 * EX] = w;
+        }
+    }
+    __syncthreads();
+    // ---- 1c. inverse stage B -> H_demag tile (the nx live cells)
+    {
+        const int pb = tid / N2, k2 = tid % N2;
+        cx<T> u[N1];
+        const cx<T>* ex = sm + (pb * N2 + k2) * EX;
+#pragma unroll
+        for (int q = 0; q < N1; ++q) u[q] = ex[q];
+        constexpr int NO = N1 == 1 ? 1 : N1 / 2;
+        DftP<N1, +1, N1, NO>::run(u);
+        __syncthreads(); // the tile overlays the exchange buffer
+        T* ha = hm + (2 * pb) * nx;
+        T* hb = ha + nx;
+#pragma unroll
+        for (int k1 = 0; k1 < NO; ++k1) {
+            const int x = k2 + N2 * k1;
+            if (x < nx) {
+                ha[x] = u[k1].x;
+                hb[x] = u[k1].y;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- 2. local terms + LLG on the tile's cells; M_{t+1} to HBM and to the tile
+    CellLLG<T> cl;
+    cl.load(ctl, coeff, kan);
+    double tmax = 0.0;
+    const int sy = nx, sz = nx * ny;
+    for (int e = tid; e < TR * nx; e += NT) {
+        const int yl = e / nx, i = e - yl * nx, j = y0 + yl;
+        if (j >= ny) continue;
+        const int f = z * sz + j * sy + i;
+        const unsigned mask = nbr_mask(i, j, z, nx, ny, nz);
+        T mc[3], ex[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const T* p = m + c * n + f;
+            T nb[6];
+            nb[0] = (mask & 1u) ? __ldg(p - 1) : T(0);
+            nb[1] = (mask & 2u) ? __ldg(p + 1) : T(0);
+            nb[2] = (mask & 4u) ? __ldg(p - sy) : T(0);
+            nb[3] = (mask & 8u) ? __ldg(p + sy) : T(0);
+            nb[4] = (mask & 16u) ? __ldg(p - sz) : T(0);
+            nb[5] = (mask & 32u) ? __ldg(p + sz) : T(0);
+            mc[c] = __ldg(p);
+            ex[c] = exch_sum6<T>(mc[c], nb, mask);
+        }
+        T hx = hm[(0 * TR + yl) * nx + i], hy = hm[(1 * TR + yl) * nx + i], hz = hm[(2 * TR + yl) * nx + i];
+        cl.heff(mc[0], hx, hy, hz, ex[0], ex[1], ex[2]);
+        bool zero = false;
+        tmax = fmax(tmax, cl.update(mc[0], mc[1], mc[2], hx, hy, hz, zero));
+        if (zero)
+            atomicMin(&ctl->bad_key, (static_cast<unsigned long long>(cur_step) << 36) |
+                                         static_cast<unsigned long long>(f));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            mout[c * n + f] = mc[c];
+            hm[(c * TR + yl) * nx + i] = mc[c];
+        }
+    }
+    __syncthreads();
+
+    // ---- 3a. forward stage A on the new tile (rows 2p, 2p+1 of one component)
+    if (a_task) {
+        const int ra = 2 * pa, rb = ra + 1;
+        const int ya = y0 + (ra % TR), yb = ya + 1;
+        const T* tra = hm + ra * nx;
+        const T* trb = hm + rb * nx;
+        const bool va = ya < ny, vb = yb < ny;
+        constexpr int NZ = N2 / 2;
+#pragma unroll
+        for (int n2 = 0; n2 < NZ; ++n2) {
+            const int x = n1 + N1 * n2;
+            const bool in = x < nx;
+            v[n2] = cx<T>{(in && va) ? tra[x] : T(0), (in && vb) ? trb[x] : T(0)};
+        }
+        DftP<N2, -1, NZ, N2>::run(v);
+    }
+    __syncthreads(); // the exchange buffer overlays the tile
+    if (a_task) {
+        cx<T>* ex = sm + (pa * N2) * EX + n1;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+            cx<T> w = v[k2];
+            if (k2 > 0) w = cmul(w, tws[k2 * N1 + n1]);
+            ex[k2 * EX] = w;
+        }
+    }
+    __syncthreads();
+    // ---- 3b. forward stage B -> natural-order Z rows
+    {
+        const int pb = tid / N2, k2 = tid % N2;
+        cx<T> u[N1];
+        const cx<T>* ex = sm + (pb * N2 + k2) * EX;
+#pragma unroll
+        for (int q = 0; q < N1; ++q) u[q] = ex[q];
+        DftP<N1, -1, N1, N1>::run(u);
+        __syncthreads();
+        cx<T>* zr = sm + pb * ZP + k2;
+#pragma unroll
+        for (int k1 = 0; k1 < N1; ++k1) zr[N2 * k1] = u[k1];
+    }
+    __syncthreads();
+    // ---- 3c. separate the packed rows, write the next step's half spectra (kx-major)
+    const T half = T(0.5);
+    for (int it = tid; it < XH * 3 * TR; it += NT) {
+        const int r = it % (3 * TR), k = it / (3 * TR);
+        const int c = r / TR, y = y0 + (r - c * TR);
+        if (y >= ny) continue;
+        const cx<T>* zr = sm + (r >> 1) * ZP;
+        const cx<T> zk = zr[k], zm = zr[(L - k) & (L - 1)];
+        const cx<T> val = (r & 1) ? cx<T>{(zk.y + zm.y) * half, (zm.x - zk.x) * half}
+                                  : cx<T>{(zk.x + zm.x) * half, (zk.y - zm.y) * half};
+        S[sf_row(k, c, z, nz, ny) + y] = val;
+    }
+
+    // ---- per-CTA torque maximum
+    __shared__ double red[NT / 32];
+    double t = tmax;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if ((tid & 31) == 0) red[tid >> 5] = t;
+    __syncthreads();
+    if (tid == 0) {
+        double b = 0.0;
+        for (int w = 0; w < NT / 32; ++w) b = fmax(b, red[w]);
+        tpart[blockIdx.y * gridDim.x + blockIdx.x] = b;
+    }
+}
+
 template <typename K>
 void set_smem(K kernel, int bytes) {
     if (bytes > 48 * 1024) {
@@ -525,7 +754,8 @@ bool fast_supported(const Geom& g) {
 template <typename T>
 void prepare_fast_kernels(const Geom& g) {
     switch (g.log2lx) {
-#define X(l) case l: set_smem(k_xf<T, l>, x_smem_bytes<T, l>()); set_smem(k_xi<T, l>, x_smem_bytes<T, l>()); break;
+#define X(l) case l: set_smem(k_xf<T, l>, x_smem_bytes<T, l>()); set_smem(k_xi<T, l>, x_smem_bytes<T, l>()); \
+                     set_smem(k_xstep<T, l>, xs_smem_bytes<T, l>()); break;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");
@@ -568,18 +798,44 @@ void launch_fast_xi(const cx<T>* S, T* h, const Geom& g, const cx<T>* tw, cudaSt
 }
 
 template <typename T>
-void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, cudaStream_t stream) {
+void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, StepCtl* ctl,
+                    const StageTable& st, int prologue, cudaStream_t stream) {
     int sb = 0;
     const int kxb = fast_yz_kxb<T>(g, &sb);
     const unsigned grid = static_cast<unsigned>((g.xh + kxb - 1) / kxb);
     switch (g.log2ly) {
 #define X(l) case l: \
-        if (g.nz == 1) k_yz<T, l, 0><<<grid, yz_threads<l>(), sb, stream>>>(S, g, tw, kt, kxb); \
-        else if constexpr (sizeof(T) == 4) k_yz<T, l, 1><<<grid, yz_threads<l>(), sb, stream>>>(S, g, tw, kt, kxb); \
+        if (g.nz == 1) k_yz<T, l, 0><<<grid, yz_threads<l>(), sb, stream>>>(S, g, tw, kt, kxb, ctl, st, prologue); \
+        else if constexpr (sizeof(T) == 4) k_yz<T, l, 1><<<grid, yz_threads<l>(), sb, stream>>>(S, g, tw, kt, kxb, ctl, st, prologue); \
         else throw std::invalid_argument("fast path: f64 needs nz == 1"); break;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Ly");
+    }
+    check_launch();
+}
+
+template <typename T>
+int fast_xstep_blocks(const Geom& g) {
+    switch (g.log2lx) {
+#define X(l) case l: return ((g.ny + XS<l>::TR - 1) / XS<l>::TR) * g.nz;
+        MMB_FAST_CASES(X)
+#undef X
+        default: throw std::invalid_argument("fast path: bad Lx");
+    }
+}
+
+template <typename T>
+void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>* tw,
+                       double exch_coeff, double aniso_coeff, StepCtl* ctl, double* tpart,
+                       cudaStream_t stream) {
+    const T coeff = static_cast<T>(exch_coeff), kan = static_cast<T>(aniso_coeff);
+    switch (g.log2lx) {
+#define X(l) case l: { const dim3 grid((g.ny + XS<l>::TR - 1) / XS<l>::TR, g.nz); \
+        k_xstep<T, l><<<grid, XS<l>::NT, xs_smem_bytes<T, l>(), stream>>>(S, m, mout, g, tw, coeff, kan, ctl, tpart); break; }
+        MMB_FAST_CASES(X)
+#undef X
+        default: throw std::invalid_argument("fast path: bad Lx");
     }
     check_launch();
 }
@@ -591,7 +847,11 @@ void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, cudaS
     template void launch_fast_xf<T>(const T*, cx<T>*, const Geom&, const cx<T>*, StepCtl*,      \
                                     const StageTable&, int, cudaStream_t);                     \
     template void launch_fast_xi<T>(const cx<T>*, T*, const Geom&, const cx<T>*, cudaStream_t); \
-    template void launch_fast_yz<T>(cx<T>*, const Geom&, const cx<T>*, const T*, cudaStream_t);
+    template void launch_fast_yz<T>(cx<T>*, const Geom&, const cx<T>*, const T*, StepCtl*,         \
+                                    const StageTable&, int, cudaStream_t);                     \
+    template int fast_xstep_blocks<T>(const Geom&);                                            \
+    template void launch_fast_xstep<T>(cx<T>*, const T*, T*, const Geom&, const cx<T>*, double, \
+                                       double, StepCtl*, double*, cudaStream_t);
 #ifndef MMB_ONLY_F64
 MMB_FINST(float)
 #endif

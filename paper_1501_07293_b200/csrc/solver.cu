@@ -141,7 +141,8 @@ public:
         twy_.alloc(g.ly);
         twz_.alloc(g.lz);
         partial_.alloc(3 * 1024);
-        tpart_.alloc(llg_blocks(g));
+        tpart_count_ = fast_ ? fast_xstep_blocks<T>(g) : llg_blocks(g);
+        tpart_.alloc(std::max(llg_blocks(g), tpart_count_));
         red_.alloc(8);
         ctl_.alloc(1);
         ck(cudaMallocHost(&ctl_host_, sizeof(StepCtl)), "cudaMallocHost");
@@ -200,6 +201,7 @@ public:
         for (int c = 0; c < 3; ++c)
             ck(cudaMemcpyAsync(m_[cur_].p + c * n, src[c], n * sizeof(T), cudaMemcpyHostToDevice, stream_),
                "set_m");
+        s_valid_ = false;
         ck(cudaStreamSynchronize(stream_), "set_m sync");
     }
 
@@ -213,6 +215,7 @@ public:
     }
 
     void step(long long n) override {
+        if (n > 0) prime();
         for (long long i = 0; i < n; ++i) {
             ensure_graph(cur_);
             ck(cudaGraphLaunch(graph_[cur_], stream_), "cudaGraphLaunch");
@@ -259,7 +262,7 @@ public:
     }
 
     double last_torque_sq() override {
-        launch_torque_partials(tpart_.p, llg_blocks(g_), ctl_.p, stream_);
+        launch_torque_partials(tpart_.p, tpart_count_, ctl_.p, stream_);
         fetch_ctl();
         double v;
         std::memcpy(&v, &ctl_host_->torque_sq_bits, sizeof(v));
@@ -350,6 +353,7 @@ public:
         std::vector<cudaEvent_t> ev(nk + 1);
         for (auto& e : ev) ck(cudaEventCreate(&e), "event");
         std::vector<double> acc(nk, 0.0);
+        prime();
         for (long long s = 0; s < n; ++s) {
             ck(cudaEventRecord(ev[0], stream_), "record");
             enqueue_step_eager(cur_, ev.data());
@@ -437,7 +441,7 @@ private:
     }
 
     std::vector<std::string> kernel_names() const {
-        if (fast_) return {"x_fwd", "yz", "x_inv", "llg"};
+        if (fast_) return {"yz", "xstep"};
         if (g_.nz == 1) return {"x_fwd", "y_mac", "x_inv", "llg"};
         return {"x_fwd", "y_fwd", "z_mac", "y_inv", "x_inv", "llg"};
     }
@@ -449,9 +453,11 @@ private:
             if (ev) ck(cudaEventRecord(ev[k++], stream_), "record");
         };
         if (fast_) {
+            // S is reused as scratch: it no longer holds the x spectrum of the current M
+            s_valid_ = false;
             launch_fast_xf<T>(m, S_.p, g_, twx_.p, ctl_.p, st_, prologue, stream_);
             mark();
-            launch_fast_yz<T>(S_.p, g_, twy_.p, kspec_.p, stream_);
+            launch_fast_yz<T>(S_.p, g_, twy_.p, kspec_.p, ctl_.p, st_, 0, stream_);
             mark();
             launch_fast_xi<T>(S_.p, h, g_, twx_.p, stream_);
             mark();
@@ -474,7 +480,23 @@ private:
         mark();
     }
 
+    // Fast path: the step starts from S = x spectrum of M_cur (kept valid across steps by the
+    // fused KXS); prime() recomputes it after anything else touched M or S.
+    void prime() {
+        if (!fast_ || s_valid_) return;
+        launch_fast_xf<T>(m_[cur_].p, S_.p, g_, twx_.p, ctl_.p, st_, 0, stream_);
+        s_valid_ = true;
+    }
+
     void enqueue_step_eager(int cur, cudaEvent_t* ev = nullptr) {
+        if (fast_) {
+            launch_fast_yz<T>(S_.p, g_, twy_.p, kspec_.p, ctl_.p, st_, 1, stream_);
+            if (ev) ck(cudaEventRecord(ev[1], stream_), "record");
+            launch_fast_xstep<T>(S_.p, m_[cur].p, m_[cur ^ 1].p, g_, twx_.p, exch_coeff_, aniso_coeff_,
+                                 ctl_.p, tpart_.p, stream_);
+            if (ev) ck(cudaEventRecord(ev[2], stream_), "record");
+            return;
+        }
         enqueue_demag(m_[cur].p, hd_.p, 1, ev);
         launch_llg<T>(0, m_[cur].p, hd_.p, m_[cur ^ 1].p, g_, exch_coeff_, aniso_coeff_, ctl_.p, tpart_.p, stream_);
         if (ev) ck(cudaEventRecord(ev[kernel_names().size()], stream_), "record");
@@ -541,6 +563,8 @@ private:
     cudaGraphExec_t graph_[2] = {nullptr, nullptr};
     int cur_ = 0;
     bool fast_ = false;
+    bool s_valid_ = false;  // fast path: S holds the x spectrum of m_[cur_]
+    int tpart_count_ = 0;
     long long step_ = 0;
     double exch_coeff_ = 0.0, aniso_coeff_ = 0.0;
 };
