@@ -527,12 +527,22 @@ __global__ void __launch_bounds__(XS<LOG2L>::NT, xs_min_blocks<T, LOG2L>())
     const long long cur_step = ctl->cur_step;
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->step = cur_step + 1;
 
-    // ---- 1a. stage the 3*TR convolved half-spectrum rows (async copies)
-    for (int it = tid; it < XH * 3 * TR; it += NT) {
-        const int r = it % (3 * TR), k = it / (3 * TR);
-        const int c = r / TR, y = y0 + (r - c * TR);
-        if (y < ny) cp_async<sizeof(cx<T>)>(sm + r * XHP + k, S + sf_row(k, c, z, nz, ny) + y);
-        else sm[r * XHP + k] = cx<T>{0, 0};
+    // ---- 1a. stage the 3*TR convolved half-spectrum rows (async copies). Each thread keeps
+    // one row r and walks kx with a fixed stride (NT is a multiple of 3*TR): no division,
+    // 32-bit element offsets.
+    static_assert(NT % (3 * TR) == 0, "thread count must be a multiple of the tile rows");
+    constexpr int KSTEP = NT / (3 * TR);
+    const int my_r = tid % (3 * TR), my_k0 = tid / (3 * TR);
+    const int my_c = my_r / TR, my_y = y0 + (my_r - my_c * TR);
+    const bool my_live = my_y < ny;
+    const int kx_stride = 3 * nz * ny;                      // S elements between kx blocks
+    const int row_off = (my_c * nz + z) * ny + my_y;        // (c, z, y) offset inside a kx block
+    {
+        cx<T>* dst = sm + my_r * XHP;
+        for (int k = my_k0; k < XH; k += KSTEP) {
+            if (my_live) cp_async<sizeof(cx<T>)>(dst + k, S + (k * kx_stride + row_off));
+            else dst[k] = cx<T>{0, 0};
+        }
     }
     stage_twiddles<T, LOG2L>(tws, tw);
     cp_async_wait_all();
@@ -601,9 +611,15 @@ __global__ void __launch_bounds__(XS<LOG2L>::NT, xs_min_blocks<T, LOG2L>())
     cl.load(ctl, coeff, kan);
     double tmax = 0.0;
     const int sy = nx, sz = nx * ny;
-    for (int e = tid; e < TR * nx; e += NT) {
-        const int yl = e / nx, i = e - yl * nx, j = y0 + yl;
-        if (j >= ny) continue;
+    // walk the tile's cells with a fixed stride, carrying (yl, i) instead of dividing
+    int yl = 0, i = tid;
+    while (i >= nx) {
+        i -= nx;
+        ++yl;
+    }
+    for (; yl < TR; ) {
+        const int j = y0 + yl;
+        if (j >= ny) break;
         const int f = z * sz + j * sy + i;
         const unsigned mask = nbr_mask(i, j, z, nx, ny, nz);
         T mc[3], ex[3];
@@ -631,6 +647,11 @@ __global__ void __launch_bounds__(XS<LOG2L>::NT, xs_min_blocks<T, LOG2L>())
         for (int c = 0; c < 3; ++c) {
             mout[c * n + f] = mc[c];
             hm[(c * TR + yl) * nx + i] = mc[c];
+        }
+        i += NT;
+        while (i >= nx) {
+            i -= nx;
+            ++yl;
         }
     }
     __syncthreads();
@@ -678,15 +699,14 @@ __global__ void __launch_bounds__(XS<LOG2L>::NT, xs_min_blocks<T, LOG2L>())
     __syncthreads();
     // ---- 3c. separate the packed rows, write the next step's half spectra (kx-major)
     const T half = T(0.5);
-    for (int it = tid; it < XH * 3 * TR; it += NT) {
-        const int r = it % (3 * TR), k = it / (3 * TR);
-        const int c = r / TR, y = y0 + (r - c * TR);
-        if (y >= ny) continue;
-        const cx<T>* zr = sm + (r >> 1) * ZP;
-        const cx<T> zk = zr[k], zm = zr[(L - k) & (L - 1)];
-        const cx<T> val = (r & 1) ? cx<T>{(zk.y + zm.y) * half, (zm.x - zk.x) * half}
-                                  : cx<T>{(zk.x + zm.x) * half, (zk.y - zm.y) * half};
-        S[sf_row(k, c, z, nz, ny) + y] = val;
+    if (my_live) {
+        const cx<T>* zr = sm + (my_r >> 1) * ZP;
+        const bool odd = my_r & 1;
+        for (int k = my_k0; k < XH; k += KSTEP) {
+            const cx<T> zk = zr[k], zm = zr[(L - k) & (L - 1)];
+            S[k * kx_stride + row_off] = odd ? cx<T>{(zk.y + zm.y) * half, (zm.x - zk.x) * half}
+                                             : cx<T>{(zk.x + zm.x) * half, (zk.y - zm.y) * half};
+        }
     }
 
     // ---- per-CTA torque maximum
