@@ -58,6 +58,7 @@ def algorithmic_bytes(nx, ny, nz, w):
     canonical = sum(k.values()) + (2 * half + tensor if nz == 1 else 2 * half + 4 * padded + tensor)
     # per-kernel algorithmic bytes of the kernels each path actually launches
     k["y_mac"] = k["yz"] = 2 * half + tensor          # fused: padded spectrum stays on chip
+    k["xstep"] = 2 * half + 6 * n * w                 # fused x^-1 + LLG + x: S in/out, M in/out
     k["y_fwd"] = half + padded
     k["z_mac"] = 2 * padded + tensor
     k["y_inv"] = padded + half

@@ -484,10 +484,10 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
 //   3. x-r2c of the new tile -> the half spectra S for the next step, in place.
 // H_demag never reaches HBM and M_{t+1} is not re-read: per step the x side moves
 // S in + S out + M_t + M_{t+1} instead of three separate passes.
-template <int LOG2L>
+template <int LOG2L, int PB = 128>
 struct XS {
     using SP = Split<LOG2L>;
-    static constexpr int P = 3 * (SP::N2 >= 128 ? 1 : 128 / SP::N2); // row pairs
+    static constexpr int P = 3 * (SP::N2 >= PB ? 1 : PB / SP::N2);   // row pairs
     static constexpr int TR = 2 * P / 3;                              // y rows per CTA
     static constexpr int NT = P * SP::N2;                             // threads
     static constexpr int XHP = ((1 << LOG2L) / 2 + 1) | 1;            // staging pitch (odd)
@@ -496,23 +496,25 @@ struct XS {
     static constexpr int A0 = 3 * TR * XHP, A1 = P * SP::N2 * EX, A2 = P * ZP;
     static constexpr int AREA = A0 > A1 ? (A0 > A2 ? A0 : A2) : (A1 > A2 ? A1 : A2);
 };
-template <typename T, int LOG2L>
+template <typename T, int LOG2L, int PB>
 constexpr int xs_smem_bytes() {
-    return (XS<LOG2L>::AREA + (1 << LOG2L)) * static_cast<int>(sizeof(cx<T>));
+    return (XS<LOG2L, PB>::AREA + (1 << LOG2L)) * static_cast<int>(sizeof(cx<T>));
 }
 
-template <typename T, int LOG2L>
+template <typename T, int LOG2L, int PB>
 constexpr int xs_min_blocks() {
     // two CTAs per SM when their shared memory fits (registers capped accordingly)
-    return 2 * xs_smem_bytes<T, LOG2L>() + 4096 <= 228 * 1024 ? 2 : 1;
+    return 2 * xs_smem_bytes<T, LOG2L, PB>() + 4096 <= 228 * 1024 ? 2 : 1;
 }
 
-template <typename T, int LOG2L>
-__global__ void __launch_bounds__(XS<LOG2L>::NT, xs_min_blocks<T, LOG2L>())
+// PB = 128: ~384 threads and 3 x 8 rows per CTA (large grids); PB = 16: 3 x 2 rows for
+// grids whose row count would otherwise leave SMs idle.
+template <typename T, int LOG2L, int PB>
+__global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>())
     k_xstep(cx<T>* __restrict__ S, const T* __restrict__ m, T* __restrict__ mout, Geom g,
             const cx<T>* __restrict__ tw, T coeff, T kan, StepCtl* ctl, double* __restrict__ tpart) {
     using SP = Split<LOG2L>;
-    using X = XS<LOG2L>;
+    using X = XS<LOG2L, PB>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = X::P, TR = X::TR, NT = X::NT;
     constexpr int XH = L / 2 + 1, XHP = X::XHP, EX = X::EX, ZP = X::ZP;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -752,10 +754,11 @@ int fast_yz_kxb(const Geom& g, int* smem_bytes) {
     const int twb = g.ly * static_cast<int>(sizeof(cx<T>));
     const int limit = 227 * 1024 - twb;
     if (per_kx > limit) return 0;
+    // as many kx per CTA as ~100 KB allows, but never fewer than ~2 CTAs per SM of work
     int kxb = (100 * 1024) / per_kx;
     if (kxb < 1) kxb = 1;
     kxb = std::min(kxb, 64);
-    kxb = std::min(kxb, g.xh);
+    kxb = std::min(kxb, std::max(1, g.xh / (2 * 148)));
     if (smem_bytes) *smem_bytes = kxb * per_kx + twb;
     return kxb;
 }
@@ -775,7 +778,8 @@ template <typename T>
 void prepare_fast_kernels(const Geom& g) {
     switch (g.log2lx) {
 #define X(l) case l: set_smem(k_xf<T, l>, x_smem_bytes<T, l>()); set_smem(k_xi<T, l>, x_smem_bytes<T, l>()); \
-                     set_smem(k_xstep<T, l>, xs_smem_bytes<T, l>()); break;
+                     set_smem(k_xstep<T, l, 128>, xs_smem_bytes<T, l, 128>()); \
+                     set_smem(k_xstep<T, l, 16>, xs_smem_bytes<T, l, 16>()); break;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");
@@ -835,10 +839,16 @@ void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, StepC
     check_launch();
 }
 
+template <int LOG2L>
+bool xstep_small(const Geom& g) {
+    return ((g.ny + XS<LOG2L, 128>::TR - 1) / XS<LOG2L, 128>::TR) * g.nz < 2 * 148;
+}
+
 template <typename T>
 int fast_xstep_blocks(const Geom& g) {
     switch (g.log2lx) {
-#define X(l) case l: return ((g.ny + XS<l>::TR - 1) / XS<l>::TR) * g.nz;
+#define X(l) case l: return xstep_small<l>(g) ? ((g.ny + XS<l, 16>::TR - 1) / XS<l, 16>::TR) * g.nz \
+                                              : ((g.ny + XS<l, 128>::TR - 1) / XS<l, 128>::TR) * g.nz;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");
@@ -851,8 +861,10 @@ void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>
                        cudaStream_t stream) {
     const T coeff = static_cast<T>(exch_coeff), kan = static_cast<T>(aniso_coeff);
     switch (g.log2lx) {
-#define X(l) case l: { const dim3 grid((g.ny + XS<l>::TR - 1) / XS<l>::TR, g.nz); \
-        k_xstep<T, l><<<grid, XS<l>::NT, xs_smem_bytes<T, l>(), stream>>>(S, m, mout, g, tw, coeff, kan, ctl, tpart); break; }
+#define X(l) case l: if (xstep_small<l>(g)) { const dim3 grid((g.ny + XS<l, 16>::TR - 1) / XS<l, 16>::TR, g.nz); \
+        k_xstep<T, l, 16><<<grid, XS<l, 16>::NT, xs_smem_bytes<T, l, 16>(), stream>>>(S, m, mout, g, tw, coeff, kan, ctl, tpart); \
+        } else { const dim3 grid((g.ny + XS<l, 128>::TR - 1) / XS<l, 128>::TR, g.nz); \
+        k_xstep<T, l, 128><<<grid, XS<l, 128>::NT, xs_smem_bytes<T, l, 128>(), stream>>>(S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");
