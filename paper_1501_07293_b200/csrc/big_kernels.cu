@@ -1,0 +1,332 @@
+// big_kernels.cu — the fast path for grids whose per-kx spectrum block does not fit in shared
+// memory (nz > 8, e.g. 1024x1024x32 and the 2048x2048x64 slabs): the y/z part of the
+// convolution is split into three streaming kernels around a padded spectrum S2:
+//
+//   KYF (k_yrow, forward): per (kx, c, z) row, y-FFT of the ny live values -> Ly values (S -> S2)
+//   KZ  (k_zmac)         : per (kx, ky) pencil tile, z-FFT (nz -> Lz, pruned), 6-component
+//                          tensor MAC, z-inverse (Lz -> nz), in place in S2
+//   KYI (k_yrow, inverse): per row, Ly -> ny live values (S2 -> S)
+//
+// then the fused KXS (fast_kernels.cu) as on the small-nz path. All row transforms are the
+// register four-step of fft4.cuh with unit-stride global loads/stores.
+#include <stdexcept>
+#include <string>
+
+#include "fast.hpp"
+#include "fast_common.cuh"
+
+namespace mmb {
+
+namespace {
+
+void check_launch() {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+template <int LOG2L>
+struct YR {
+    using SP = Split<LOG2L>;
+    static constexpr int P = SP::N2 >= 256 ? 1 : 256 / SP::N2; // rows per CTA
+    static constexpr int NT = P * SP::N2;
+    static constexpr int EX = SP::N1 + 1;
+};
+template <typename T, int LOG2L>
+constexpr int yr_smem_bytes() {
+    using Y = YR<LOG2L>;
+    return (Y::P * Split<LOG2L>::N2 * Y::EX + (1 << LOG2L)) * static_cast<int>(sizeof(cx<T>));
+}
+
+// Row FFT along y. INV = 0: in rows hold n_live values (pitch in_pitch), out rows get all L
+// values. INV = 1: in rows hold L values, out rows get the first n_live values.
+template <typename T, int LOG2L, int INV>
+__global__ void __launch_bounds__(YR<LOG2L>::NT)
+    k_yrow(const cx<T>* __restrict__ in, cx<T>* __restrict__ out, long long nrows, int in_pitch,
+           int out_pitch, int n_live, const cx<T>* __restrict__ tw, StepCtl* ctl, StageTable st,
+           int prologue) {
+    using SP = Split<LOG2L>;
+    constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = YR<LOG2L>::P, EX = YR<LOG2L>::EX;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
+    cx<T>* tws = sm + P * N2 * EX;
+    if (prologue && blockIdx.x == 0 && threadIdx.x == 0) step_prologue(ctl, st, prologue);
+    stage_twiddles<T, LOG2L>(tws, tw);
+    __syncthreads();
+    const int tid = threadIdx.x;
+    const long long r0 = static_cast<long long>(blockIdx.x) * P;
+    if (tid < P * N1) {
+        const int p = tid / N1, n1 = tid % N1;
+        const long long r = r0 + p;
+        cx<T> v[N2];
+        if (r < nrows) {
+            const cx<T>* src = in + r * in_pitch;
+            if constexpr (!INV) {
+                constexpr int NZ = N2 / 2;
+#pragma unroll
+                for (int n2 = 0; n2 < NZ; ++n2) {
+                    const int y = n1 + N1 * n2;
+                    v[n2] = y < n_live ? src[y] : cx<T>{0, 0};
+                }
+                DftP<N2, -1, NZ, N2>::run(v);
+            } else {
+#pragma unroll
+                for (int n2 = 0; n2 < N2; ++n2) v[n2] = src[n1 + N1 * n2];
+                DftP<N2, +1, N2, N2>::run(v);
+            }
+        } else {
+#pragma unroll
+            for (int n2 = 0; n2 < N2; ++n2) v[n2] = cx<T>{0, 0};
+        }
+        cx<T>* ex = sm + (p * N2) * EX + n1;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+            cx<T> w = v[k2];
+            if (k2 > 0) w = INV ? cmulc(w, tws[k2 * N1 + n1]) : cmul(w, tws[k2 * N1 + n1]);
+            ex[k2 * EX] = w;
+        }
+    }
+    __syncthreads();
+    {
+        const int p = tid / N2, k2 = tid % N2;
+        const long long r = r0 + p;
+        if (r < nrows) {
+            cx<T> u[N1];
+            const cx<T>* ex = sm + (p * N2 + k2) * EX;
+#pragma unroll
+            for (int q = 0; q < N1; ++q) u[q] = ex[q];
+            cx<T>* dst = out + r * out_pitch;
+            if constexpr (!INV) {
+                DftP<N1, -1, N1, N1>::run(u);
+#pragma unroll
+                for (int k1 = 0; k1 < N1; ++k1) dst[k2 + N2 * k1] = u[k1];
+            } else {
+                constexpr int NO = N1 == 1 ? 1 : N1 / 2;
+                DftP<N1, +1, N1, NO>::run(u);
+#pragma unroll
+                for (int k1 = 0; k1 < NO; ++k1) {
+                    const int y = k2 + N2 * k1;
+                    if (y < n_live) dst[y] = u[k1];
+                }
+            }
+        }
+    }
+}
+
+// z pencils: W consecutive ky of one kx, all three components, Lz = 2^LOG2LZ >= 2 nz - 1.
+template <typename T>
+constexpr int zw() { return sizeof(T) == 4 ? 32 : 16; }
+constexpr int kZThreads = 256;
+template <typename T, int LOG2LZ>
+constexpr int z_smem_bytes() {
+    return (2 * 3 * (1 << LOG2LZ) * zw<T>() + (1 << LOG2LZ)) * static_cast<int>(sizeof(cx<T>));
+}
+
+template <typename T, int LOG2LZ>
+__global__ void __launch_bounds__(kZThreads)
+    k_zmac(cx<T>* __restrict__ S2, Geom g, const cx<T>* __restrict__ tw, const T* __restrict__ kt) {
+    using SP = Split<LOG2LZ>;
+    constexpr int LZ = SP::L, N1 = SP::N1, N2 = SP::N2, W = zw<T>();
+    constexpr int CS = LZ * W; // component stride in a tile buffer
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cx<T>* A = reinterpret_cast<cx<T>*>(smem_raw); // [c][z][w]
+    cx<T>* B = A + 3 * CS;
+    cx<T>* tws = B + 3 * CS;
+    const int kx = blockIdx.y, ky0 = blockIdx.x * W;
+    const int nz = g.nz, ly = g.ly, yh = g.yh, zh = g.zh;
+    const int wl = min(W, ly - ky0);
+    const int tid = threadIdx.x;
+    const long long zpitch = ly;
+    const cx<T>* base = S2 + static_cast<long long>(kx) * 3 * nz * ly + ky0;
+
+    // load the live planes (async, coalesced over ky), zero the padding planes
+    for (int e = tid; e < 3 * LZ * W; e += kZThreads) {
+        const int w = e % W, zc = e / W, c = zc / LZ, z = zc % LZ;
+        if (z < nz && w < wl) cp_async<sizeof(cx<T>)>(A + e, base + (c * nz + z) * zpitch + w);
+        else A[e] = cx<T>{0, 0};
+    }
+    stage_twiddles<T, LOG2LZ>(tws, tw);
+    cp_async_wait_all();
+    __syncthreads();
+
+    // z forward, stage A: task (c, n1, w), w fastest; inputs z >= nz are zero (pruned)
+    for (int t = tid; t < 3 * N1 * W; t += kZThreads) {
+        const int w = t % W, cn = t / W, c = cn / N1, n1 = cn % N1;
+        cx<T> v[N2];
+        const cx<T>* src = A + c * CS + w;
+        constexpr int NZ = N2 / 2 > 0 ? N2 / 2 : 1;
+#pragma unroll
+        for (int n2 = 0; n2 < NZ; ++n2) v[n2] = src[(n1 + N1 * n2) * W];
+        DftP<N2, -1, NZ, N2>::run(v);
+        cx<T>* dst = B + c * CS + w;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+            cx<T> x = v[k2];
+            if (k2 > 0) x = cmul(x, tws[k2 * N1 + n1]);
+            dst[(k2 * N1 + n1) * W] = x;
+        }
+    }
+    __syncthreads();
+    // z forward, stage B -> natural kz in A
+    for (int t = tid; t < 3 * N2 * W; t += kZThreads) {
+        const int w = t % W, ck = t / W, c = ck / N2, k2 = ck % N2;
+        cx<T> u[N1];
+        const cx<T>* src = B + c * CS + (k2 * N1) * W + w;
+#pragma unroll
+        for (int q = 0; q < N1; ++q) u[q] = src[q * W];
+        DftP<N1, -1, N1, N1>::run(u);
+        cx<T>* dst = A + c * CS + w;
+#pragma unroll
+        for (int k1 = 0; k1 < N1; ++k1) dst[(k2 + N2 * k1) * W] = u[k1];
+    }
+    __syncthreads();
+    // tensor MAC per (kz, ky)
+    for (int t = tid; t < LZ * W; t += kZThreads) {
+        const int w = t % W, kz = t / W;
+        if (w >= wl) continue;
+        const int ky = ky0 + w;
+        const bool fy = 2 * ky > ly, fz = 2 * kz > LZ;
+        const int kyo = fy ? ly - ky : ky, kzo = fz ? LZ - kz : kz;
+        T k6[6];
+        load6<T>(kt + ((static_cast<long long>(kx) * zh + kzo) * yh + kyo) * 6, k6);
+        if (fy) k6[1] = -k6[1];
+        if (fz) k6[2] = -k6[2];
+        if (fy != fz) k6[4] = -k6[4];
+        cx<T>* p = A + kz * W + w;
+        cx<T> a = p[0], b = p[CS], c = p[2 * CS];
+        mac3<T>(k6, a, b, c);
+        p[0] = a;
+        p[CS] = b;
+        p[2 * CS] = c;
+    }
+    __syncthreads();
+    // z inverse, stage A (all inputs)
+    for (int t = tid; t < 3 * N1 * W; t += kZThreads) {
+        const int w = t % W, cn = t / W, c = cn / N1, n1 = cn % N1;
+        cx<T> v[N2];
+        const cx<T>* src = A + c * CS + w;
+#pragma unroll
+        for (int n2 = 0; n2 < N2; ++n2) v[n2] = src[(n1 + N1 * n2) * W];
+        DftP<N2, +1, N2, N2>::run(v);
+        cx<T>* dst = B + c * CS + w;
+#pragma unroll
+        for (int k2 = 0; k2 < N2; ++k2) {
+            cx<T> x = v[k2];
+            if (k2 > 0) x = cmulc(x, tws[k2 * N1 + n1]);
+            dst[(k2 * N1 + n1) * W] = x;
+        }
+    }
+    __syncthreads();
+    // z inverse, stage B: the nz live planes back to S2
+    cx<T>* obase = S2 + static_cast<long long>(kx) * 3 * nz * ly + ky0;
+    for (int t = tid; t < 3 * N2 * W; t += kZThreads) {
+        const int w = t % W, ck = t / W, c = ck / N2, k2 = ck % N2;
+        cx<T> u[N1];
+        const cx<T>* src = B + c * CS + (k2 * N1) * W + w;
+#pragma unroll
+        for (int q = 0; q < N1; ++q) u[q] = src[q * W];
+        constexpr int NO = N1 == 1 ? 1 : N1 / 2;
+        DftP<N1, +1, N1, NO>::run(u);
+        if (w < wl) {
+#pragma unroll
+            for (int k1 = 0; k1 < NO; ++k1) {
+                const int z = k2 + N2 * k1;
+                if (z < nz) obase[(c * nz + z) * zpitch + w] = u[k1];
+            }
+        }
+    }
+}
+
+template <typename K>
+void set_smem(K kernel, int bytes) {
+    if (bytes > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    }
+}
+
+#define MMB_Y_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12)
+#define MMB_Z_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7)
+
+} // namespace
+
+template <typename T>
+bool big_supported(const Geom& g) {
+    if (g.lx < 2 || g.ly < 2 || g.nz < 2) return false;
+    if (g.log2lx > 12 || g.log2ly > 12 || g.log2lz > 7) return false;
+    if (sizeof(T) == 8 && (g.log2lx > 10 || g.log2ly > 10)) return false; // DFT_64 f64 spills
+    return true;
+}
+
+template <typename T>
+void prepare_big_kernels(const Geom& g) {
+    switch (g.log2ly) {
+#define X(l) case l: set_smem(k_yrow<T, l, 0>, yr_smem_bytes<T, l>()); set_smem(k_yrow<T, l, 1>, yr_smem_bytes<T, l>()); break;
+        MMB_Y_CASES(X)
+#undef X
+        default: throw std::invalid_argument("big path: bad Ly");
+    }
+    switch (g.log2lz) {
+#define X(l) case l: set_smem(k_zmac<T, l>, z_smem_bytes<T, l>()); break;
+        MMB_Z_CASES(X)
+#undef X
+        default: throw std::invalid_argument("big path: bad Lz");
+    }
+}
+
+template <typename T>
+void launch_big_yf(const cx<T>* S, cx<T>* S2, const Geom& g, const cx<T>* tw, StepCtl* ctl,
+                   const StageTable& st, int prologue, cudaStream_t stream) {
+    const long long nrows = static_cast<long long>(g.xh) * 3 * g.nz;
+    switch (g.log2ly) {
+#define X(l) case l: { constexpr int P = YR<l>::P; \
+        k_yrow<T, l, 0><<<static_cast<unsigned>((nrows + P - 1) / P), YR<l>::NT, yr_smem_bytes<T, l>(), stream>>>( \
+            S, S2, nrows, g.ny, g.ly, g.ny, tw, ctl, st, prologue); break; }
+        MMB_Y_CASES(X)
+#undef X
+        default: throw std::invalid_argument("big path: bad Ly");
+    }
+    check_launch();
+}
+
+template <typename T>
+void launch_big_yi(const cx<T>* S2, cx<T>* S, const Geom& g, const cx<T>* tw, cudaStream_t stream) {
+    const long long nrows = static_cast<long long>(g.xh) * 3 * g.nz;
+    StageTable st{};
+    switch (g.log2ly) {
+#define X(l) case l: { constexpr int P = YR<l>::P; \
+        k_yrow<T, l, 1><<<static_cast<unsigned>((nrows + P - 1) / P), YR<l>::NT, yr_smem_bytes<T, l>(), stream>>>( \
+            S2, S, nrows, g.ly, g.ny, g.ny, tw, nullptr, st, 0); break; }
+        MMB_Y_CASES(X)
+#undef X
+        default: throw std::invalid_argument("big path: bad Ly");
+    }
+    check_launch();
+}
+
+template <typename T>
+void launch_big_z(cx<T>* S2, const Geom& g, const cx<T>* tw, const T* kt, cudaStream_t stream) {
+    switch (g.log2lz) {
+#define X(l) case l: { const dim3 grid((g.ly + zw<T>() - 1) / zw<T>(), g.xh); \
+        k_zmac<T, l><<<grid, kZThreads, z_smem_bytes<T, l>(), stream>>>(S2, g, tw, kt); break; }
+        MMB_Z_CASES(X)
+#undef X
+        default: throw std::invalid_argument("big path: bad Lz");
+    }
+    check_launch();
+}
+
+#define MMB_BINST(T)                                                                              \
+    template bool big_supported<T>(const Geom&);                                                 \
+    template void prepare_big_kernels<T>(const Geom&);                                           \
+    template void launch_big_yf<T>(const cx<T>*, cx<T>*, const Geom&, const cx<T>*, StepCtl*,     \
+                                   const StageTable&, int, cudaStream_t);                        \
+    template void launch_big_yi<T>(const cx<T>*, cx<T>*, const Geom&, const cx<T>*, cudaStream_t); \
+    template void launch_big_z<T>(cx<T>*, const Geom&, const cx<T>*, const T*, cudaStream_t);
+#ifndef MMB_ONLY_F64
+MMB_BINST(float)
+#endif
+#ifndef MMB_ONLY_F32
+MMB_BINST(double)
+#endif
+
+} // namespace mmb

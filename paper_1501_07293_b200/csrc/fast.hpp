@@ -35,4 +35,16 @@ template <typename T>
 void launch_tensor_finalize_fast(const double* spec, T* out, int xh, int yh, int zh, double scale,
                                  cudaStream_t stream);
 
+// ---- nz > 8 (or blocks too large for shared memory): y and z as streaming kernels around a
+// padded spectrum S2[kx][c][z][Ly] (big_kernels.cu).
+template <typename T> bool big_supported(const Geom& g);
+template <typename T> void prepare_big_kernels(const Geom& g);
+template <typename T>
+void launch_big_yf(const cx<T>* S, cx<T>* S2, const Geom& g, const cx<T>* tw, StepCtl* ctl,
+                   const StageTable& st, int prologue, cudaStream_t stream);
+template <typename T>
+void launch_big_z(cx<T>* S2, const Geom& g, const cx<T>* tw, const T* kt, cudaStream_t stream);
+template <typename T>
+void launch_big_yi(const cx<T>* S2, cx<T>* S, const Geom& g, const cx<T>* tw, cudaStream_t stream);
+
 } // namespace mmb

@@ -1,0 +1,82 @@
+// fast_common.cuh — device helpers shared by the fast-path kernels: kx-major spectrum row
+// addressing, Ampere async copies, Hopper/Blackwell TMA bulk copies with mbarriers, packed
+// tensor loads and shared-memory twiddle staging.
+#pragma once
+
+#include "fft4.cuh"
+#include "types.cuh"
+
+namespace mmb {
+
+__device__ __forceinline__ long long sf_row(int kx, int c, int z, int nz, int ny) {
+    return ((static_cast<long long>(kx) * 3 + c) * nz + z) * ny;
+}
+
+// Ampere-style async global->shared copy of one element (LDGSTS), bypassing registers.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// ---- TMA (cp.async.bulk) global -> shared with an mbarrier transaction count
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// six tensor coefficients stored contiguously ([..][6]): three 2-vector loads
+template <typename T>
+__device__ __forceinline__ void load6(const T* __restrict__ p, T (&k)[6]) {
+    const cx<T>* q = reinterpret_cast<const cx<T>*>(p);
+    const cx<T> a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+    k[0] = a.x;
+    k[1] = a.y;
+    k[2] = b.x;
+    k[3] = b.y;
+    k[4] = c.x;
+    k[5] = c.y;
+}
+
+// Stage-A twiddles W_L^{n1*k2} staged in shared memory as [k2][n1] (unit stride across the
+// n1-consecutive lanes of stage A: bank-conflict free, no global loads on the hot path).
+template <typename T, int LOG2L>
+__device__ __forceinline__ void stage_twiddles(cx<T>* tws, const cx<T>* __restrict__ tw) {
+    using SP = Split<LOG2L>;
+    for (int e = threadIdx.x; e < SP::L; e += blockDim.x) {
+        const int k2 = e / SP::N1, n1 = e % SP::N1;
+        tws[e] = __ldg(&tw[n1 * k2]);
+    }
+}
+
+
+} // namespace mmb

@@ -126,8 +126,26 @@ public:
             throw std::invalid_argument("mmb: more than 715M cells per device (32-bit cell indexing)");
         g.rows = static_cast<long long>(d.ny) * d.nz;
 
+        // Path: fused y/z in shared memory (nz <= 8; z padded to Lz = 16, which gives the same
+        // linear convolution as any L >= 2nz-1), streaming y/z kernels for larger blocks, or
+        // the general pipeline (MMB_GENERAL_PATH=1 forces it, for parity testing).
         const char* force_general = std::getenv("MMB_GENERAL_PATH");
-        fast_ = fast_supported<T>(g) && !(force_general && force_general[0] == '1');
+        const bool allow_fast = !(force_general && force_general[0] == '1');
+        Geom gy = g;
+        if (gy.nz >= 2 && gy.nz <= 8) {
+            gy.lz = 16;
+            gy.log2lz = 4;
+            gy.zh = 9;
+        }
+        const char* force_big = std::getenv("MMB_BIG_PATH");
+        const bool allow_yz = !(force_big && force_big[0] == '1');
+        if (allow_fast && allow_yz && fast_supported<T>(gy)) {
+            g = gy;
+            fast_ = yz_ = true;
+        } else if (allow_fast && big_supported<T>(g)) {
+            fast_ = true;
+            yz_ = false;
+        }
 
         const size_t n = static_cast<size_t>(g.n);
         m_[0].alloc(3 * n);
@@ -136,6 +154,7 @@ public:
         heff_.alloc(3 * n);
         S_.alloc(fast_ ? static_cast<size_t>(3) * g.nz * g.ny * g.xh
                       : static_cast<size_t>(3) * g.nz * g.ly * g.xp);
+        if (fast_ && !yz_) S2_.alloc(static_cast<size_t>(3) * g.nz * g.ly * g.xh);
         kspec_.alloc(static_cast<size_t>(6) * g.zh * g.yh * g.xh);
         twx_.alloc(g.lx);
         twy_.alloc(g.ly);
@@ -152,6 +171,7 @@ public:
         launch_twiddles<T>(twz_.p, g.lz, stream_);
         if (fast_) prepare_fast_kernels<T>(g_);
         else prepare_fft_kernels<T>(g_);
+        if (fast_ && !yz_) prepare_big_kernels<T>(g_);
 
         // StepCtl: step 0, alpha from the material (llg.cpp:31-33).
         StepCtl c{};
@@ -380,7 +400,7 @@ public:
     int launches_per_step() const override { return static_cast<int>(kernel_names().size()); }
 
     size_t device_bytes() const override {
-        return m_[0].bytes() + m_[1].bytes() + hd_.bytes() + heff_.bytes() + S_.bytes() +
+        return m_[0].bytes() + m_[1].bytes() + hd_.bytes() + heff_.bytes() + S_.bytes() + S2_.bytes() +
                kspec_.bytes() + twx_.bytes() + twy_.bytes() + twz_.bytes() + partial_.bytes() +
                red_.bytes() + tpart_.bytes() + ctl_.bytes();
     }
@@ -441,7 +461,8 @@ private:
     }
 
     std::vector<std::string> kernel_names() const {
-        if (fast_) return {"yz", "xstep"};
+        if (fast_ && yz_) return {"yz", "xstep"};
+        if (fast_) return {"y_fwd", "z_mac", "y_inv", "xstep"};
         if (g_.nz == 1) return {"x_fwd", "y_mac", "x_inv", "llg"};
         return {"x_fwd", "y_fwd", "z_mac", "y_inv", "x_inv", "llg"};
     }
@@ -457,8 +478,7 @@ private:
             s_valid_ = false;
             launch_fast_xf<T>(m, S_.p, g_, twx_.p, ctl_.p, st_, prologue, stream_);
             mark();
-            launch_fast_yz<T>(S_.p, g_, twy_.p, kspec_.p, ctl_.p, st_, 0, stream_);
-            mark();
+            enqueue_yz(0, ev ? &k : nullptr, ev);
             launch_fast_xi<T>(S_.p, h, g_, twx_.p, stream_);
             mark();
             return;
@@ -488,13 +508,32 @@ private:
         s_valid_ = true;
     }
 
+    // y/z part of the fast path on S (fused KYZ, or KYF/KZ/KYI through S2); `k` indexes
+    // the profiling events.
+    void enqueue_yz(int prologue, int* k, cudaEvent_t* ev) {
+        auto mark = [&]() {
+            if (ev && k) ck(cudaEventRecord(ev[(*k)++], stream_), "record");
+        };
+        if (yz_) {
+            launch_fast_yz<T>(S_.p, g_, twy_.p, kspec_.p, ctl_.p, st_, prologue, stream_);
+            mark();
+            return;
+        }
+        launch_big_yf<T>(S_.p, S2_.p, g_, twy_.p, ctl_.p, st_, prologue, stream_);
+        mark();
+        launch_big_z<T>(S2_.p, g_, twz_.p, kspec_.p, stream_);
+        mark();
+        launch_big_yi<T>(S2_.p, S_.p, g_, twy_.p, stream_);
+        mark();
+    }
+
     void enqueue_step_eager(int cur, cudaEvent_t* ev = nullptr) {
         if (fast_) {
-            launch_fast_yz<T>(S_.p, g_, twy_.p, kspec_.p, ctl_.p, st_, 1, stream_);
-            if (ev) ck(cudaEventRecord(ev[1], stream_), "record");
+            int k = 1;
+            enqueue_yz(1, &k, ev);
             launch_fast_xstep<T>(S_.p, m_[cur].p, m_[cur ^ 1].p, g_, twx_.p, exch_coeff_, aniso_coeff_,
                                  ctl_.p, tpart_.p, stream_);
-            if (ev) ck(cudaEventRecord(ev[2], stream_), "record");
+            if (ev) ck(cudaEventRecord(ev[k], stream_), "record");
             return;
         }
         enqueue_demag(m_[cur].p, hd_.p, 1, ev);
@@ -555,7 +594,7 @@ private:
     StageTable st_{};
     cudaStream_t stream_ = nullptr;
     DevBuf<T> m_[2], hd_, heff_;
-    DevBuf<cx<T>> S_, twx_, twy_, twz_;
+    DevBuf<cx<T>> S_, S2_, twx_, twy_, twz_;
     DevBuf<T> kspec_;
     DevBuf<double> partial_, red_, tpart_;
     DevBuf<StepCtl> ctl_;
@@ -563,6 +602,7 @@ private:
     cudaGraphExec_t graph_[2] = {nullptr, nullptr};
     int cur_ = 0;
     bool fast_ = false;
+    bool yz_ = false;       // fast path with the fused shared-memory y/z kernel
     bool s_valid_ = false;  // fast path: S holds the x spectrum of m_[cur_]
     int tpart_count_ = 0;
     long long step_ = 0;

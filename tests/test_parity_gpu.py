@@ -24,19 +24,23 @@ GOLD = os.path.join(HERE, "golden")
 TOL_H = {"f64": 1e-12, "f32": 1e-5}
 
 
-@pytest.fixture(params=["fast", "general"])
+@pytest.fixture(params=["fast", "big", "general"])
 def path(request, monkeypatch):
-    """Both demag paths: the fused fast path (where supported) and the general pipeline."""
+    """All demag paths: the fused shared-memory y/z kernel (where supported), the streaming
+    y/z kernels (MMB_BIG_PATH=1; natural for nz > 8) and the general pipeline."""
+    monkeypatch.delenv("MMB_GENERAL_PATH", raising=False)
+    monkeypatch.delenv("MMB_BIG_PATH", raising=False)
     if request.param == "general":
         monkeypatch.setenv("MMB_GENERAL_PATH", "1")
-    else:
-        monkeypatch.delenv("MMB_GENERAL_PATH", raising=False)
+    elif request.param == "big":
+        monkeypatch.setenv("MMB_BIG_PATH", "1")
     return request.param
 
 GRIDS = [
     (1, 1, 1, 2.0), (2, 2, 2, 1.0), (3, 3, 3, 2.0), (4, 4, 2, 1.0), (5, 3, 2, 3.0), (7, 1, 1, 1.0),
     (1, 6, 2, 1.0), (8, 8, 4, 1.0), (6, 5, 3, 1.0), (16, 12, 3, 2.5), (33, 17, 1, 3.0),
     (128, 32, 1, 3.90625), (166, 42, 1, 3.0), (40, 24, 9, 2.0), (64, 64, 1, 1.0), (1, 1, 17, 1.0),
+    (24, 20, 33, 1.5), (32, 16, 12, 1.0),
 ]
 
 
