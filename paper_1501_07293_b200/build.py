@@ -30,7 +30,7 @@ COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relax
 UNITS = [
     ("fft_f32.o", "fft_kernels.cu", ["-DMMB_ONLY_F32"]),
     ("fft_f64.o", "fft_kernels.cu", ["-DMMB_ONLY_F64"]),
-    ("fast_f32.o", "fast_kernels.cu", ["-DMMB_ONLY_F32"]),
+    ("fast_f32.o", "fast_kernels.cu", ["-DMMB_ONLY_F32"] + os.environ.get("MMB_XFLAGS", "").split()),
     ("fast_f64.o", "fast_kernels.cu", ["-DMMB_ONLY_F64"]),
     ("big_f32.o", "big_kernels.cu", ["-DMMB_ONLY_F32"]),
     ("big_f64.o", "big_kernels.cu", ["-DMMB_ONLY_F64"]),

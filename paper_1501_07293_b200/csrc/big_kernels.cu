@@ -124,6 +124,10 @@ constexpr int z_smem_bytes() {
 template <typename T, int LOG2LZ>
 __global__ void __launch_bounds__(kZThreads)
     k_zmac(cx<T>* __restrict__ S2, Geom g, const cx<T>* __restrict__ tw, const T* __restrict__ kt) {
+    // Lz = N1*N2. Forward: stage A (DFT_N2 over n2 per (c, n1)), then the fused middle: per
+    // (k2, ky) all three components in registers, DFT_N1 -> kz = k2 + N2 k1 natural, tensor
+    // MAC, inverse DFT_N1, conj twiddle; then inverse stage A' (IDFT_N2 per (c, n1)) straight
+    // to the nz live planes. Two shared buffers (A: [c][z][w], B: exchange), three barriers.
     using SP = Split<LOG2LZ>;
     constexpr int LZ = SP::L, N1 = SP::N1, N2 = SP::N2, W = zw<T>();
     constexpr int CS = LZ * W; // component stride in a tile buffer
@@ -136,101 +140,98 @@ __global__ void __launch_bounds__(kZThreads)
     const int wl = min(W, ly - ky0);
     const int tid = threadIdx.x;
     const long long zpitch = ly;
-    const cx<T>* base = S2 + static_cast<long long>(kx) * 3 * nz * ly + ky0;
+    cx<T>* blk = S2 + static_cast<long long>(kx) * 3 * nz * ly + ky0;
 
-    // load the live planes (async, coalesced over ky), zero the padding planes
-    for (int e = tid; e < 3 * LZ * W; e += kZThreads) {
-        const int w = e % W, zc = e / W, c = zc / LZ, z = zc % LZ;
-        if (z < nz && w < wl) cp_async<sizeof(cx<T>)>(A + e, base + (c * nz + z) * zpitch + w);
-        else A[e] = cx<T>{0, 0};
+    // load the nz live planes (async, coalesced over ky)
+    for (int e = tid; e < 3 * nz * W; e += kZThreads) {
+        const int w = e % W, cz = e / W, c = cz / nz, z = cz - c * nz;
+        cx<T>* d = A + (c * LZ + z) * W + w;
+        if (w < wl) cp_async<sizeof(cx<T>)>(d, blk + (c * nz + z) * zpitch + w);
+        else *d = cx<T>{0, 0};
     }
     stage_twiddles<T, LOG2LZ>(tws, tw);
     cp_async_wait_all();
     __syncthreads();
 
-    // z forward, stage A: task (c, n1, w), w fastest; inputs z >= nz are zero (pruned)
+    // forward stage A: task (c, n1, w); planes z >= nz are zero (pruned, never read)
     for (int t = tid; t < 3 * N1 * W; t += kZThreads) {
         const int w = t % W, cn = t / W, c = cn / N1, n1 = cn % N1;
+        constexpr int NZ = N2 / 2 > 0 ? N2 / 2 : 1;
         cx<T> v[N2];
         const cx<T>* src = A + c * CS + w;
-        constexpr int NZ = N2 / 2 > 0 ? N2 / 2 : 1;
 #pragma unroll
-        for (int n2 = 0; n2 < NZ; ++n2) v[n2] = src[(n1 + N1 * n2) * W];
+        for (int n2 = 0; n2 < NZ; ++n2) {
+            const int z = n1 + N1 * n2;
+            v[n2] = z < nz ? src[z * W] : cx<T>{0, 0};
+        }
         DftP<N2, -1, NZ, N2>::run(v);
-        cx<T>* dst = B + c * CS + w;
+        cx<T>* dst = B + c * CS + n1 * W + w;
 #pragma unroll
         for (int k2 = 0; k2 < N2; ++k2) {
             cx<T> x = v[k2];
             if (k2 > 0) x = cmul(x, tws[k2 * N1 + n1]);
-            dst[(k2 * N1 + n1) * W] = x;
+            dst[k2 * N1 * W] = x;
         }
     }
     __syncthreads();
-    // z forward, stage B -> natural kz in A
-    for (int t = tid; t < 3 * N2 * W; t += kZThreads) {
-        const int w = t % W, ck = t / W, c = ck / N2, k2 = ck % N2;
-        cx<T> u[N1];
-        const cx<T>* src = B + c * CS + (k2 * N1) * W + w;
+
+    // fused middle: task (k2, w)
+    for (int t = tid; t < N2 * W; t += kZThreads) {
+        const int w = t % W, k2 = t / W;
+        cx<T> u[3][N1];
 #pragma unroll
-        for (int q = 0; q < N1; ++q) u[q] = src[q * W];
-        DftP<N1, -1, N1, N1>::run(u);
-        cx<T>* dst = A + c * CS + w;
+        for (int c = 0; c < 3; ++c) {
+            const cx<T>* src = B + c * CS + (k2 * N1) * W + w;
 #pragma unroll
-        for (int k1 = 0; k1 < N1; ++k1) dst[(k2 + N2 * k1) * W] = u[k1];
+            for (int q = 0; q < N1; ++q) u[c][q] = src[q * W];
+            DftP<N1, -1, N1, N1>::run(u[c]);
+        }
+        if (w < wl) {
+            const int ky = ky0 + w;
+            const bool fy = 2 * ky > ly;
+            const int kyo = fy ? ly - ky : ky;
+            const T* kb = kt + (static_cast<long long>(kx) * zh * yh + kyo) * 6;
+#pragma unroll
+            for (int k1 = 0; k1 < N1; ++k1) {
+                const int kz = k2 + N2 * k1;
+                const bool fz = 2 * kz > LZ;
+                const int kzo = fz ? LZ - kz : kz;
+                T k6[6];
+                load6<T>(kb + static_cast<long long>(kzo) * yh * 6, k6);
+                if (fy) k6[1] = -k6[1];
+                if (fz) k6[2] = -k6[2];
+                if (fy != fz) k6[4] = -k6[4];
+                mac3<T>(k6, u[0][k1], u[1][k1], u[2][k1]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            DftP<N1, +1, N1, N1>::run(u[c]);
+            cx<T>* dst = A + c * CS + (k2 * N1) * W + w;
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) {
+                cx<T> x = u[c][n1];
+                if (k2 > 0) x = cmulc(x, tws[k2 * N1 + n1]);
+                dst[n1 * W] = x;
+            }
+        }
     }
     __syncthreads();
-    // tensor MAC per (kz, ky)
-    for (int t = tid; t < LZ * W; t += kZThreads) {
-        const int w = t % W, kz = t / W;
-        if (w >= wl) continue;
-        const int ky = ky0 + w;
-        const bool fy = 2 * ky > ly, fz = 2 * kz > LZ;
-        const int kyo = fy ? ly - ky : ky, kzo = fz ? LZ - kz : kz;
-        T k6[6];
-        load6<T>(kt + ((static_cast<long long>(kx) * zh + kzo) * yh + kyo) * 6, k6);
-        if (fy) k6[1] = -k6[1];
-        if (fz) k6[2] = -k6[2];
-        if (fy != fz) k6[4] = -k6[4];
-        cx<T>* p = A + kz * W + w;
-        cx<T> a = p[0], b = p[CS], c = p[2 * CS];
-        mac3<T>(k6, a, b, c);
-        p[0] = a;
-        p[CS] = b;
-        p[2 * CS] = c;
-    }
-    __syncthreads();
-    // z inverse, stage A (all inputs)
+
+    // inverse stage A': task (c, n1, w), IDFT_N2 over k2, the nz live planes to S2
     for (int t = tid; t < 3 * N1 * W; t += kZThreads) {
         const int w = t % W, cn = t / W, c = cn / N1, n1 = cn % N1;
         cx<T> v[N2];
-        const cx<T>* src = A + c * CS + w;
+        const cx<T>* src = A + c * CS + n1 * W + w;
 #pragma unroll
-        for (int n2 = 0; n2 < N2; ++n2) v[n2] = src[(n1 + N1 * n2) * W];
-        DftP<N2, +1, N2, N2>::run(v);
-        cx<T>* dst = B + c * CS + w;
-#pragma unroll
-        for (int k2 = 0; k2 < N2; ++k2) {
-            cx<T> x = v[k2];
-            if (k2 > 0) x = cmulc(x, tws[k2 * N1 + n1]);
-            dst[(k2 * N1 + n1) * W] = x;
-        }
-    }
-    __syncthreads();
-    // z inverse, stage B: the nz live planes back to S2
-    cx<T>* obase = S2 + static_cast<long long>(kx) * 3 * nz * ly + ky0;
-    for (int t = tid; t < 3 * N2 * W; t += kZThreads) {
-        const int w = t % W, ck = t / W, c = ck / N2, k2 = ck % N2;
-        cx<T> u[N1];
-        const cx<T>* src = B + c * CS + (k2 * N1) * W + w;
-#pragma unroll
-        for (int q = 0; q < N1; ++q) u[q] = src[q * W];
-        constexpr int NO = N1 == 1 ? 1 : N1 / 2;
-        DftP<N1, +1, N1, NO>::run(u);
+        for (int k2 = 0; k2 < N2; ++k2) v[k2] = src[k2 * N1 * W];
+        constexpr int NO = N2 / 2 > 0 ? N2 / 2 : 1;
+        DftP<N2, +1, N2, NO>::run(v);
         if (w < wl) {
 #pragma unroll
-            for (int k1 = 0; k1 < NO; ++k1) {
-                const int z = k2 + N2 * k1;
-                if (z < nz) obase[(c * nz + z) * zpitch + w] = u[k1];
+            for (int n2 = 0; n2 < NO; ++n2) {
+                const int z = n1 + N1 * n2;
+                if (z < nz) blk[(c * nz + z) * zpitch + w] = v[n2];
             }
         }
     }
