@@ -128,6 +128,22 @@ int mmb_launches_per_step(mmb_ctx* ctx, int* out);
 /* Bytes of device memory held by the handle. */
 int mmb_device_bytes(mmb_ctx* ctx, size_t* out);
 
+/* ---- multi-GPU: z-slab decomposition ------------------------------------
+ * One process per GPU. Rank 0 creates an NCCL id with mmb_nccl_unique_id and shares it (e.g.
+ * via torch.distributed broadcast); every rank then calls mmb_create_sharded with its rank.
+ * The handle owns the z-slab [z0, z0+nz_local) (mmb_slab): set_m/get_m exchange that slab
+ * (SoA, nz_local planes); step/run/average/last_torque_sq are collective (all ranks call
+ * them in the same order); <m> is the global average. Field hooks (energy, max_torque,
+ * effective_field, demag_field, tensor) are single-device only. mmb_create_emulated runs all
+ * `world` ranks of the same decomposition on this process's device (exchanges by device
+ * copies) and exposes the whole grid — used to test the sharded pipeline on one GPU. */
+int mmb_nccl_unique_id(unsigned char out[128]);
+int mmb_create_sharded(const mmb_desc* desc, const mmb_stage* stages, int nstages, int rank,
+                       int world, const unsigned char nccl_id[128], mmb_ctx** out);
+int mmb_create_emulated(const mmb_desc* desc, const mmb_stage* stages, int nstages, int world,
+                        mmb_ctx** out);
+int mmb_slab(mmb_ctx* ctx, int* z0, int* nz_local);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

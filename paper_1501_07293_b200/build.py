@@ -23,8 +23,27 @@ BUILD = os.path.join(ROOT, "build", "mmb")
 LIB = os.path.join(HERE, "libmmb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir():
+    """The NCCL that torch loads (nvidia-nccl wheel), so one libnccl.so.2 serves both in a
+    process; the system NCCL only when the wheel is absent."""
+    try:
+        import nvidia  # namespace package of the CUDA wheels
+        for base in nvidia.__path__:
+            d = os.path.join(base, "nccl")
+            if os.path.exists(os.path.join(d, "lib", "libnccl.so.2")):
+                return d
+    except ImportError:
+        pass
+    return None
+
+
+NCCL_DIR = _nccl_dir()
 COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-Xptxas", "-warn-spills", f"-I{os.path.join(ROOT, 'include')}"]
+if NCCL_DIR:
+    COMMON = COMMON[:-1] + [f"-I{os.path.join(NCCL_DIR, 'include')}"] + COMMON[-1:]
 
 # (object name, source, extra flags)
 UNITS = [
@@ -37,6 +56,7 @@ UNITS = [
     ("llg.o", "llg_kernels.cu", ["--fmad=false"]),
     ("tensor.o", "tensor_kernels.cu", ["--fmad=false"]),
     ("solver.o", "solver.cu", []),
+    ("shard.o", "shard.cu", []),
 ]
 
 
@@ -76,7 +96,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         results = list(ex.map(lambda u: _compile(u, force, verbose), UNITS))
     objs = [o for o, _ in results]
     if force or any(changed for _, changed in results) or not os.path.exists(LIB):
-        cmd = [NVCC] + ARCH + ["-shared", "-Xlinker", "-soname=libmmb.so", "-o", LIB] + objs + ["-lcudart"]
+        nccl = (["-L" + os.path.join(NCCL_DIR, "lib"), "-Xlinker", "-l:libnccl.so.2", "-Xlinker", "-rpath", "-Xlinker", os.path.join(NCCL_DIR, "lib")]
+                if NCCL_DIR else ["-lnccl"])
+        cmd = [NVCC] + ARCH + ["-shared", "-Xlinker", "-soname=libmmb.so", "-o", LIB] + objs + ["-lcudart"] + nccl
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

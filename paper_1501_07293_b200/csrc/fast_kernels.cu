@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
     const int y0 = blockIdx.x * (2 * P), z = blockIdx.y, c = blockIdx.z;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
     const int tid = threadIdx.x;
-    const T* plane = m + (static_cast<long long>(c) * nz + z) * ny * nx;
+    const T* plane = m + c * g.cs + static_cast<long long>(z) * ny * nx;
 
     // stage A: task (p, n1), n1 fastest; inputs beyond nx (and rows beyond ny) are zero
     if (tid < P * N1) {
@@ -455,7 +455,8 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
 
     const int y0 = blockIdx.x * TR, z = blockIdx.y;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
-    const int n = static_cast<int>(g.n);
+    const long long cs = g.cs;
+    const int zg = g.z0 + z, nzg = g.nz_g;
     const int tid = threadIdx.x;
     const long long cur_step = ctl->cur_step;
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->step = cur_step + 1;
@@ -554,11 +555,11 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
         const int j = y0 + yl;
         if (j >= ny) break;
         const int f = z * sz + j * sy + i;
-        const unsigned mask = nbr_mask(i, j, z, nx, ny, nz);
+        const unsigned mask = nbr_mask(i, j, zg, nx, ny, nzg);
         T mc[3], ex[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const T* p = m + c * n + f;
+            const T* p = m + c * cs + f;
             T nb[6];
             nb[0] = (mask & 1u) ? __ldg(p - 1) : T(0);
             nb[1] = (mask & 2u) ? __ldg(p + 1) : T(0);
@@ -575,10 +576,10 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
         tmax = fmax(tmax, cl.update(mc[0], mc[1], mc[2], hx, hy, hz, zero));
         if (zero)
             atomicMin(&ctl->bad_key, (static_cast<unsigned long long>(cur_step) << 36) |
-                                         static_cast<unsigned long long>(f));
+                                         static_cast<unsigned long long>(f + static_cast<long long>(g.z0) * sz));
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            mout[c * n + f] = mc[c];
+            mout[c * cs + f] = mc[c];
             hm[(c * TR + yl) * nx + i] = mc[c];
         }
         i += NT;

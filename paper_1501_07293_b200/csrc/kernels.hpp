@@ -41,9 +41,10 @@ void launch_llg(int mode, const T* m, const T* hd, T* out, const Geom& g, double
 // ctl->torque_sq_bits.
 int llg_blocks(const Geom& g);
 void launch_torque_partials(const double* tpart, int nb, StepCtl* ctl, cudaStream_t stream);
-// Deterministic fp64 sums of M components: partial[nblk*3] then out[3] (sum, not mean).
+// Deterministic fp64 sums of the n cells of each M component (component stride cs):
+// partial[nblk*3] then out[3] (sum, not mean).
 template <typename T>
-void launch_sum3(const T* m, long long n, double* partial, double* out, cudaStream_t stream);
+void launch_sum3(const T* m, long long n, long long cs, double* partial, double* out, cudaStream_t stream);
 // max_cell |M x H|^2 in fp64 -> *out_bits (double bits, atomicMax).
 template <typename T>
 void launch_torque_max(const T* m, const T* h, long long n, unsigned long long* out_bits,

@@ -164,13 +164,13 @@ __global__ void k_torque_partials(const double* __restrict__ tpart, int nb, Step
 // Block-partial fp64 sums of the three components in a fixed order.
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_sum3(const T* __restrict__ m, long long n,
-                                                      double* __restrict__ partial) {
+                                                      long long cs, double* __restrict__ partial) {
     double s[3] = {0.0, 0.0, 0.0};
     for (long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; f < n;
          f += static_cast<long long>(gridDim.x) * blockDim.x) {
         s[0] += double(__ldg(m + f));
-        s[1] += double(__ldg(m + n + f));
-        s[2] += double(__ldg(m + 2 * n + f));
+        s[1] += double(__ldg(m + cs + f));
+        s[2] += double(__ldg(m + 2 * cs + f));
     }
     __shared__ double red[3][kRedThreads / 32];
     for (int c = 0; c < 3; ++c) {
@@ -330,9 +330,9 @@ void launch_llg(int mode, const T* m, const T* hd, T* out, const Geom& g, double
 }
 
 template <typename T>
-void launch_sum3(const T* m, long long n, double* partial, double* out, cudaStream_t stream) {
+void launch_sum3(const T* m, long long n, long long cs, double* partial, double* out, cudaStream_t stream) {
     const int nb = reduce_blocks(n);
-    k_sum3<T><<<nb, kRedThreads, 0, stream>>>(m, n, partial);
+    k_sum3<T><<<nb, kRedThreads, 0, stream>>>(m, n, cs, partial);
     k_final_sum<3><<<1, 96, 0, stream>>>(partial, nb, out);
     check_launch();
 }
@@ -363,7 +363,7 @@ void launch_tensor_octant(double* E, int nx, int ny, int nz, double delta, cudaS
 #define MMB_INST(T)                                                                                 \
     template void launch_llg<T>(int, const T*, const T*, T*, const Geom&, double, double, StepCtl*, \
                                 double*, cudaStream_t);                                            \
-    template void launch_sum3<T>(const T*, long long, double*, double*, cudaStream_t);              \
+    template void launch_sum3<T>(const T*, long long, long long, double*, double*, cudaStream_t);   \
     template void launch_torque_max<T>(const T*, const T*, long long, unsigned long long*,          \
                                        cudaStream_t);                                              \
     template void launch_energy<T>(const T*, const T*, const Geom&, double, const StepCtl*,         \

@@ -20,70 +20,9 @@
 #include "../../include/mmb.h"
 #include "fast.hpp"
 #include "kernels.hpp"
+#include "solver_base.hpp"
 
 namespace mmb {
-
-struct numerical_error : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-struct cuda_error : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-
-static void ck(cudaError_t e, const char* what) {
-    if (e == cudaErrorMemoryAllocation) throw std::bad_alloc();
-    if (e != cudaSuccess) throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-static int pow2_at_least(int v) {
-    int l = 1;
-    while (l < v) l <<= 1;
-    return l;
-}
-static int ilog2(int v) {
-    int r = 0;
-    while ((1 << r) < v) ++r;
-    return r;
-}
-
-template <typename T>
-struct DevBuf {
-    T* p = nullptr;
-    size_t n = 0;
-    void alloc(size_t count) {
-        n = count;
-        if (count) ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
-    }
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
-    size_t bytes() const { return n * sizeof(T); }
-};
-
-class SolverBase {
-public:
-    virtual ~SolverBase() = default;
-    virtual int precision() const = 0;
-    virtual void set_m(const void*, const void*, const void*) = 0;
-    virtual void get_m(void*, void*, void*) = 0;
-    virtual void step(long long n) = 0;
-    virtual long long step_index() const = 0;
-    virtual void average(double* out) = 0;
-    virtual double energy() = 0;
-    virtual double max_torque() = 0;
-    virtual double last_torque_sq() = 0;
-    virtual long long run(long long steps, long long cadence, double stop_torque,
-                          mmb_record_fn fn, void* user) = 0;
-    virtual void synchronize() = 0;
-    virtual void effective_field(void*, void*, void*) = 0;
-    virtual void demag_field(const void*, const void*, const void*, void*, void*, void*) = 0;
-    virtual void tensor_octant(double*) = 0;
-    virtual void upload_tensor_octant(const double*) = 0;
-    virtual float time_steps(long long n) = 0;
-    virtual int profile_step(long long n, float* ms, int maxk, std::string& names) = 0;
-    virtual int launches_per_step() const = 0;
-    virtual size_t device_bytes() const = 0;
-};
 
 template <typename T>
 class Solver final : public SolverBase {
@@ -125,6 +64,9 @@ public:
         if (3 * g.n >= (1LL << 31))
             throw std::invalid_argument("mmb: more than 715M cells per device (32-bit cell indexing)");
         g.rows = static_cast<long long>(d.ny) * d.nz;
+        g.cs = g.n;
+        g.nz_g = g.nz;
+        g.z0 = 0;
 
         // Path: fused y/z in shared memory (nz <= 8; z padded to Lz = 16, which gives the same
         // linear convolution as any L >= 2nz-1), streaming y/z kernels for larger blocks, or
@@ -248,7 +190,7 @@ public:
 
     void average(double* out) override {
         // average_magnetization (vector_field.hpp:86-99) / average_unit (llg.cpp:126-131)
-        launch_sum3<T>(m_[cur_].p, g_.n, partial_.p, red_.p, stream_);
+        launch_sum3<T>(m_[cur_].p, g_.n, g_.n, partial_.p, red_.p, stream_);
         double s[3];
         ck(cudaMemcpyAsync(s, red_.p, sizeof(s), cudaMemcpyDeviceToHost, stream_), "average");
         sync_and_check();
@@ -398,6 +340,11 @@ public:
     }
 
     int launches_per_step() const override { return static_cast<int>(kernel_names().size()); }
+
+    void slab(int& z0, int& nzl) const override {
+        z0 = 0;
+        nzl = g_.nz;
+    }
 
     size_t device_bytes() const override {
         return m_[0].bytes() + m_[1].bytes() + hd_.bytes() + heff_.bytes() + S_.bytes() + S2_.bytes() +
@@ -790,6 +737,41 @@ int mmb_profile_step(mmb_ctx* ctx, long long n, float* kernel_ms, int max_kernel
 int mmb_launches_per_step(mmb_ctx* ctx, int* out) {
     if (!ctx || !out) return bad("mmb_launches_per_step");
     *out = ctx->s->launches_per_step();
+    return MMB_OK;
+}
+
+int mmb_nccl_unique_id(unsigned char out[128]) {
+    if (!out) return bad("mmb_nccl_unique_id");
+    return guarded([&] { mmb::nccl_unique_id(out); return MMB_OK; });
+}
+
+int mmb_create_sharded(const mmb_desc* desc, const mmb_stage* stages, int nstages, int rank,
+                       int world, const unsigned char nccl_id[128], mmb_ctx** out) {
+    if (!desc || !out || !nccl_id) return bad("mmb_create_sharded");
+    *out = nullptr;
+    return guarded([&] {
+        auto h = std::make_unique<mmb_ctx>();
+        h->s = mmb::make_sharded(*desc, stages, nstages, rank, world, nccl_id);
+        *out = h.release();
+        return MMB_OK;
+    });
+}
+
+int mmb_create_emulated(const mmb_desc* desc, const mmb_stage* stages, int nstages, int world,
+                        mmb_ctx** out) {
+    if (!desc || !out) return bad("mmb_create_emulated");
+    *out = nullptr;
+    return guarded([&] {
+        auto h = std::make_unique<mmb_ctx>();
+        h->s = mmb::make_emulated(*desc, stages, nstages, world);
+        *out = h.release();
+        return MMB_OK;
+    });
+}
+
+int mmb_slab(mmb_ctx* ctx, int* z0, int* nz_local) {
+    if (!ctx || !z0 || !nz_local) return bad("mmb_slab");
+    ctx->s->slab(*z0, *nz_local);
     return MMB_OK;
 }
 

@@ -49,6 +49,11 @@ struct Geom {
     int yh, zh;                 // tensor octant extents (Ly/2+1, Lz/2+1)
     long long n;                // nx*ny*nz
     long long rows;             // ny*nz (real rows per component)
+    // M/H buffer addressing (slab decomposition): component stride of the M buffers in
+    // elements, the global plane count and this slab's first global plane. A single-device
+    // solver has cs = n, nz_g = nz, z0 = 0.
+    long long cs;
+    int nz_g, z0;
 };
 
 __host__ __device__ inline long long s_index(const Geom& g, int c, int z, int ky, int kx) {

@@ -70,7 +70,8 @@ class Simulation:
     """Simulation<T> on one B200: state (M ping-pong, spectral scratch, tensor spectrum) lives
     in HBM; step() enqueues one CUDA-graph replay of the fused per-step kernels."""
 
-    def __init__(self, spec: ProblemSpec, precision: Precision = Precision.f64, device: int = 0):
+    def __init__(self, spec: ProblemSpec, precision: Precision = Precision.f64, device: int = 0,
+                 _create=None):
         spec.material.validate()
         self._spec = spec
         self._precision = precision
@@ -87,8 +88,14 @@ class Simulation:
                                    (C.c_double * 3)(*s.field_end), int(s.alpha_override is not None),
                                    float(s.alpha_override or 0.0))
         self._h = C.c_void_p()
-        _lib.check(L.mmb_create(C.byref(desc), arr, len(stages), C.byref(self._h)))
         self._L = L
+        if _create is None:
+            _lib.check(L.mmb_create(C.byref(desc), arr, len(stages), C.byref(self._h)))
+        else:
+            _lib.check(_create(L, C.byref(desc), arr, len(stages), C.byref(self._h)))
+        z0, nzl = C.c_int(), C.c_int()
+        _lib.check(L.mmb_slab(self._h, C.byref(z0), C.byref(nzl)))
+        self.z0, self.nz_local = z0.value, nzl.value
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -156,7 +163,8 @@ class Simulation:
 
     # ---- state access (Simulation<T>::magnetization) ---------------------------------------
     def _shape(self):
-        return (3,) + self._spec.grid.shape
+        g = self._spec.grid
+        return (3, self.nz_local, g.ny, g.nx)
 
     def magnetization(self) -> np.ndarray:
         out = np.empty(self._shape(), dtype=self.dtype)
@@ -222,6 +230,30 @@ class Simulation:
         v = C.c_size_t()
         _lib.check(self._L.mmb_device_bytes(self._h, C.byref(v)))
         return v.value
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id (rank 0 creates it; broadcast it to the other ranks)."""
+    buf = C.create_string_buffer(128)
+    _lib.check(_lib.load().mmb_nccl_unique_id(buf))
+    return buf.raw
+
+
+def make_sharded_simulation(spec: ProblemSpec, precision: Precision, rank: int, world: int,
+                            nccl_id: bytes, device: int = 0) -> Simulation:
+    """One rank of the z-slab decomposition (one process per GPU, NCCL exchanges). The
+    handle's magnetization() / set_magnetization() cover its slab [z0, z0 + nz_local)."""
+    def create(L, desc, arr, n, out):
+        return L.mmb_create_sharded(desc, arr, n, rank, world, nccl_id, out)
+    return Simulation(spec, precision, device, _create=create)
+
+
+def make_emulated_sharded_simulation(spec: ProblemSpec, precision: Precision, world: int,
+                                     device: int = 0) -> Simulation:
+    """All `world` ranks of the decomposition on one device (device-copy exchanges)."""
+    def create(L, desc, arr, n, out):
+        return L.mmb_create_emulated(desc, arr, n, world, out)
+    return Simulation(spec, precision, device, _create=create)
 
 
 def make_simulation(spec: ProblemSpec, backend: Backend = Backend.b200,

@@ -291,3 +291,56 @@ def test_reference_side_adapter_runs():
         pytest.skip("adapter binary not built (CPU suite builds it where /root/reference exists)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------- slab decomposition
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("grid,world", [((40, 24, 9, 2.0), 2), ((40, 24, 9, 2.0), 3),
+                                        ((32, 16, 8, 1.0), 2), ((24, 20, 33, 1.5), 4),
+                                        ((16, 12, 4, 2.5), 4)])
+def test_sharded_pipeline_equals_single_device(grid, world, prec, monkeypatch):
+    """The z-slab decomposition (all-to-all transposes, per-rank column y/z kernels, halo
+    exchange, slab KXS) run as `world` emulated ranks on this GPU reproduces the single-device
+    solver on the same path bitwise, through a ramp stage and the sticky alpha override."""
+    from paper_1501_07293_b200 import Precision
+    from paper_1501_07293_b200.simulation import make_emulated_sharded_simulation
+    nx, ny, nz, delta = grid
+    sp = spec(nx, ny, nz, delta, 1.3e7, 800.0, 30.0, 0.5, 5e-6,
+              [(0, 6, (10.0, -20.0, 5.0)), (6, 12, (0.0, 50.0, 0.0), True, (40.0, 0.0, 0.0), 0.1)])
+    dt = np.float64 if prec == "f64" else np.float32
+    rng = np.random.default_rng(3 + nz)
+    v = rng.uniform(-1, 1, (3, nz, ny, nx))
+    m0 = (800.0 * v / np.sqrt((v * v).sum(0))).astype(dt)
+    if nz > 8:
+        monkeypatch.setenv("MMB_BIG_PATH", "1")  # same y/z path as the sharded solver
+    single = b200(sp, prec)
+    single.set_magnetization(m0)
+    single.step(12)
+    shard = make_emulated_sharded_simulation(sp, Precision.f64 if prec == "f64" else Precision.f32, world)
+    shard.set_magnetization(m0)
+    shard.step(12)
+    a, b = shard.magnetization(), single.magnetization()
+    assert np.array_equal(a, b), rel(a, b)
+    assert np.allclose(shard.average_unit(), single.average_unit(), rtol=0, atol=1e-12)
+    assert abs(shard.last_torque_sq() - single.last_torque_sq()) <= 1e-12 * single.last_torque_sq()
+
+
+def test_nccl_sharded_single_rank_matches_single_device(monkeypatch):
+    """The NCCL-backed sharded handle (one rank: communicator init, self transposes, NCCL
+    all-reduce of <m>) reproduces the single-device solver bitwise."""
+    from paper_1501_07293_b200 import Precision
+    from paper_1501_07293_b200.simulation import make_sharded_simulation, nccl_unique_id
+    sp = spec(24, 20, 12, 1.5, 1.3e7, 800.0, 30.0, 0.5, 5e-6, [(0, 100, (10.0, -20.0, 5.0))])
+    monkeypatch.setenv("MMB_BIG_PATH", "1")
+    single = b200(sp, "f32")
+    rng = np.random.default_rng(11)
+    v = rng.uniform(-1, 1, (3, 12, 20, 24))
+    m0 = (800.0 * v / np.sqrt((v * v).sum(0))).astype(np.float32)
+    single.set_magnetization(m0)
+    single.step(8)
+    sh = make_sharded_simulation(sp, Precision.f32, 0, 1, nccl_unique_id())
+    assert (sh.z0, sh.nz_local) == (0, 12)
+    sh.set_magnetization(m0)
+    sh.step(8)
+    assert np.array_equal(sh.magnetization(), single.magnetization())
+    assert np.allclose(sh.average_unit(), single.average_unit(), rtol=0, atol=1e-12)
