@@ -36,7 +36,10 @@ WORKLOADS = {
     "256x256x1_f32": (256, 256, 1, 3.0, 1.3e7, 800.0, 0.0, 0.5, 5e-6, "f32"),
     "256x256x1_f64": (256, 256, 1, 3.0, 1.3e7, 800.0, 0.0, 0.5, 5e-6, "f64"),
     "sp4_128x32x1_f64": (128, 32, 1, 3.90625, 1.3e7, 800.0, 0.0, 0.5, 5e-6, "f64"),
+    # BASELINE configs[4]: slab-sharded across the GPUs of the box (strong scaling)
+    "2048x2048x64_f32": (2048, 2048, 64, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5, "f32"),
 }
+SHARDED = {"2048x2048x64_f32"}
 METRIC = "LLG cell-updates/s"
 UNIT = "cell-updates/s"
 
@@ -232,7 +235,79 @@ def run_reference(args, world, rank):
     return 0
 
 
+def run_b200_sharded(args, world, rank, local):
+    """BASELINE configs[4]: one global grid split into z-slabs over the ranks (NCCL transposes
+    and halo exchange); value = global cell-updates / max-over-ranks device time."""
+    from paper_1501_07293_b200 import Grid, MaterialParams, Precision, ProblemSpec
+    from paper_1501_07293_b200.simulation import make_sharded_simulation, nccl_unique_id
+    import torch
+    import torch.distributed as dist
+    wl = args.workload
+    nx, ny, nz, delta, a_ex, ms, hk, alpha, dt, prec = WORKLOADS[wl]
+    w = 4 if prec == "f32" else 8
+    n = nx * ny * nz
+    nid = torch.zeros(128, dtype=torch.uint8, device="cuda" if world > 1 else "cpu")
+    if rank == 0:
+        nid[:] = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8)
+    if world > 1:
+        dist.broadcast(nid, 0)
+    spec = ProblemSpec(name=wl, grid=Grid(nx, ny, nz, delta), material=MaterialParams(a_ex, ms, hk, alpha), dt=dt)
+    sim = make_sharded_simulation(spec, Precision.f32 if prec == "f32" else Precision.f64, rank, world,
+                                  bytes(nid.cpu().numpy()), device=local)
+    rng = np.random.default_rng(20240 + rank)
+    v = rng.uniform(-1.0, 1.0, (3, sim.nz_local, ny, nx)).astype(np.float32)
+    v /= np.maximum(np.sqrt((v * v).sum(0)), 0.1)
+    sim.set_magnetization((ms * v).astype(np.float32 if prec == "f32" else np.float64))
+    del v
+    sim.time_steps(max(3, args.warmup))
+    barrier(world)
+    with ClockSampler(local) as clk:
+        t_ms = sim.time_steps(args.steps)
+    t_ms = max_over_ranks(world, t_ms)
+    value = n * args.steps / (t_ms * 1e-3)
+    ms_step = t_ms / args.steps
+    b_alg, _ = algorithmic_bytes(nx, ny, nz, w)
+    peak, peak_kind = load_peaks()
+    achieved = b_alg / (ms_step * 1e-3) / 1e9
+    # e2e: each rank moves its slab host->device and back around every step
+    pin = torch.empty((3, sim.nz_local, ny, nx), dtype=torch.float32 if prec == "f32" else torch.float64,
+                      pin_memory=True).numpy()
+    sim.get_m_into(pin)
+    e_steps = max(1, min(args.steps, 5))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        sim.set_m_from(pin)
+        sim.step(1)
+        sim.get_m_into(pin)
+    te = max_over_ranks(world, time.perf_counter() - t0)
+    slab_bytes = 3 * sim.nz_local * ny * nx * w
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+                "config": {"workload": wl, "nx": nx, "ny": ny, "nz": nz, "delta_nm": delta,
+                           "parallelism": f"z-slabs x{world} (NCCL all-to-all transposes + halo)",
+                           "l2": "working set >> 126 MB L2; no flush", "cells": n},
+                "roofline": {"bound": "hbm", "kernel": "sharded_step", "achieved": achieved / world,
+                             "peak": peak, "unit": "GB/s", "frac": achieved / world / peak, "traffic": None,
+                             "alg_bytes": b_alg, "peak_kind": peak_kind,
+                             "note": "canonical step bytes (SURVEY §8(d)) per GPU over the step time"},
+                "cpu_baseline": {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                                 "sample": "N/A: the reference layout needs ~181 GB at 2048x2048x64 (SURVEY §8(d))"},
+                "e2e": {"value": n * e_steps / te, "unit": UNIT, "h2d_bytes_per_step": slab_bytes * world,
+                        "d2h_bytes_per_step": slab_bytes * world,
+                        "api": "mmb_set_m + mmb_step(1) + mmb_get_m per step on every rank's slab"},
+                "gpu_launches": sim.launches_per_step() * args.steps,
+                "clocks": clk.summary(), "device_bytes": sim.device_bytes()}
+        print(json.dumps(line), flush=True)
+    barrier(world)
+    return 0
+
+
 def run_b200(args, world, rank, local):
+    if args.workload in SHARDED:
+        return run_b200_sharded(args, world, rank, local)
     from paper_1501_07293_b200 import (Grid, MaterialParams, Precision, ProblemSpec, make_simulation)
     import torch
     wl = args.workload

@@ -418,7 +418,9 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
 template <int LOG2L, int PB = 128>
 struct XS {
     using SP = Split<LOG2L>;
-    static constexpr int P = 3 * (SP::N2 >= PB ? 1 : PB / SP::N2);   // row pairs
+    // Lx = 4096 halves the tile so exchange buffer + twiddle table stay within 227 KB
+    static constexpr int PBE = (LOG2L >= 12 && PB > 16) ? PB / 2 : PB;
+    static constexpr int P = 3 * (SP::N2 >= PBE ? 1 : PBE / SP::N2);  // row pairs
     static constexpr int TR = 2 * P / 3;                              // y rows per CTA
     static constexpr int NT = P * SP::N2;                             // threads
     static constexpr int XHP = ((1 << LOG2L) / 2 + 1) | 1;            // staging pitch (odd)
