@@ -10,7 +10,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SHORT = {"k_xf": "x_fwd", "k_yz": "yz", "k_xi": "x_inv", "k_llg": "llg", "k_x_fwd": "x_fwd",
-         "k_x_inv": "x_inv", "k_y_mac": "y_mac", "k_z_mac": "z_mac"}
+         "k_x_inv": "x_inv", "k_y_mac": "y_mac", "k_z_mac": "z_mac", "k_xstep": "xstep",
+         "k_zmac": "z_mac"}
 METRICS = [
     ("gpu__time_duration.sum", "time"),
     ("dram__bytes_read.sum", "dram_read"),
@@ -30,7 +31,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "
 
 def short_name(full):
     base = full.split("(")[0].split("::")[-1].split("<")[0].strip()
-    if base.startswith("k_y<") or base == "k_y":
+    if base.startswith("k_y<") or base == "k_y" or base == "k_yrow":
         return "y_inv" if ", 1>" in full.split("(")[0] else "y_fwd"
     return SHORT.get(base, base)
 
@@ -95,7 +96,10 @@ def main(tag, workload, rep, launch_csv=None):
         ls = launches(launch_csv)
         lines += ["", "# launch list (gpu__time_duration.sum, us), setup then steps:"]
         lines += [f"{n}\t{t:.2f}" for n, t in ls]
-        steps = [x for x in ls if x[0] in ("x_fwd", "yz", "x_inv", "llg", "y_fwd", "z_mac", "y_inv", "y_mac")]
+        kinds = ("x_fwd", "yz", "x_inv", "llg", "y_fwd", "z_mac", "y_inv", "y_mac", "xstep")
+        steps = [x for x in ls if x[0] in kinds]
+        if any(n == "xstep" for n, _ in steps):  # fast path: x_fwd only primes once
+            steps = [x for x in steps if x[0] != "x_fwd"]
         tot = sum(t for _, t in steps)
         share = {}
         for n, t in steps:
