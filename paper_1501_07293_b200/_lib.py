@@ -6,7 +6,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmmb.so")
+LIB_PATH = os.environ.get("MMB_LIB", os.path.join(HERE, "libmmb.so"))  # override: variants
 
 MMB_OK, MMB_ERROR_ARGUMENT, MMB_ERROR_CONFIG, MMB_ERROR_NUMERICAL = 0, 1, 2, 3
 MMB_ERROR_IO, MMB_ERROR_NOMEM, MMB_ERROR_VALIDATION, MMB_ERROR_INTERNAL, MMB_ERROR_CUDA = 4, 5, 6, 7, 8

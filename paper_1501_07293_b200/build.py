@@ -19,8 +19,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(ROOT, "build", "mmb")
-LIB = os.path.join(HERE, "libmmb.so")
+# MMB_BUILD_DIR / MMB_LIB_OUT build a variant library elsewhere (tuning experiments only)
+BUILD = os.environ.get("MMB_BUILD_DIR", os.path.join(ROOT, "build", "mmb"))
+LIB = os.environ.get("MMB_LIB_OUT", os.path.join(HERE, "libmmb.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

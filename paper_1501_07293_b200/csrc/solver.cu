@@ -9,6 +9,7 @@
 // contract (exceptions mapped to status codes as proj/src/capi.cpp:31-58 does).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -114,6 +115,9 @@ public:
         if (fast_) prepare_fast_kernels<T>(g_);
         else prepare_fft_kernels<T>(g_);
         if (fast_ && !yz_) prepare_big_kernels<T>(g_);
+        if (const char* v = std::getenv("MMB_VERBOSE"); v && v[0] == '1')
+            std::fprintf(stderr, "mmb: %dx%dx%d L=%dx%dx%d path=%s\n", d.nx, d.ny, d.nz, g.lx, g.ly, g.lz,
+                         yz_ ? "yz" : (fast_ ? "big" : "general"));
 
         // StepCtl: step 0, alpha from the material (llg.cpp:31-33).
         StepCtl c{};
