@@ -19,13 +19,13 @@ void launch_fast_xf(const T* m, cx<T>* S, const Geom& g, const cx<T>* tw, StepCt
 // KYZ; block 0 optionally runs the step prologue (schedule, sticky alpha, prefactors).
 template <typename T>
 void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, StepCtl* ctl,
-                    const StageTable& st, int prologue, cudaStream_t stream);
+                    const StageTable& st, int prologue, cudaStream_t stream, bool pdl = false);
 // KXS: fused x-c2r -> local terms + LLG update (M -> mout) -> x-r2c of mout, S in place.
 // Writes one torque partial per CTA (fast_xstep_blocks of them) to tpart.
 template <typename T>
 void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>* tw,
                        double exch_coeff, double aniso_coeff, StepCtl* ctl, double* tpart,
-                       cudaStream_t stream);
+                       cudaStream_t stream, bool pdl = false);
 template <typename T> int fast_xstep_blocks(const Geom& g);
 template <typename T>
 void launch_fast_xi(const cx<T>* S, T* h, const Geom& g, const cx<T>* tw, cudaStream_t stream);

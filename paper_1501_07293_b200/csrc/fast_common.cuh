@@ -12,6 +12,12 @@ __device__ __forceinline__ long long sf_row(int kx, int c, int z, int nz, int ny
     return ((static_cast<long long>(kx) * 3 + c) * nz + z) * ny;
 }
 
+// Programmatic dependent launch: let the next kernel in the stream start launching (its CTAs
+// take SMs as this grid's last wave drains), and wait for the previous kernel's completion and
+// memory before touching its outputs. Both are no-ops for a launch without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // Ampere-style async global->shared copy of one element (LDGSTS), bypassing registers.
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {

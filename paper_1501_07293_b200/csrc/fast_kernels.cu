@@ -12,6 +12,7 @@
 //
 // Replaces proj/src/demag.cpp:67-145 (pad, 3 forward FFTs, MAC, 3 inverse FFTs, window
 // extract). 1/(Lx Ly Lz) is folded into the tensor spectrum (tensor_kernels.cu).
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -236,6 +237,8 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
     const int nz = g.nz, ny = g.ny, xh = g.xh;
     cx<T>* tws = sm + kxb * 3 * nz * RP;
     __shared__ __align__(8) unsigned long long bar;
+    pdl_wait();
+    pdl_trigger(); // after the wait: at most one kernel ahead of the running one
     if (prologue && blockIdx.x == 0 && threadIdx.x == 0) step_prologue(ctl, st, prologue);
     const int kx0 = blockIdx.x * kxb;
     const int kxn = min(kxb, xh - kx0);
@@ -460,6 +463,8 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
     const long long cs = g.cs;
     const int zg = g.z0 + z, nzg = g.nz_g;
     const int tid = threadIdx.x;
+    pdl_wait();
+    pdl_trigger(); // after the wait: at most one kernel ahead of the running one
     const long long cur_step = ctl->cur_step;
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->step = cur_step + 1;
 
@@ -659,6 +664,32 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
     }
 }
 
+// Launch, with the programmatic-stream-serialization attribute (PDL; see pdl_wait) when
+// `pdl`: the kernel may start launching while its predecessor in the stream drains. Measured
+// to pay for multi-wave grids at one CTA per SM and to cost time on small grids, so the caller
+// decides (Solver: large grids only; MMB_NO_PDL=1 disables it everywhere).
+template <typename... KArgs, typename... Args>
+void launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                Args... args) {
+    static const bool env_off = [] {
+        const char* e = std::getenv("MMB_NO_PDL");
+        return e && e[0] == '1';
+    }();
+    const bool off = env_off || !pdl;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = off ? 0 : 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
 template <typename K>
 void set_smem(K kernel, int bytes) {
     if (bytes > 48 * 1024) {
@@ -757,14 +788,14 @@ void launch_fast_xi(const cx<T>* S, T* h, const Geom& g, const cx<T>* tw, cudaSt
 
 template <typename T>
 void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, StepCtl* ctl,
-                    const StageTable& st, int prologue, cudaStream_t stream) {
+                    const StageTable& st, int prologue, cudaStream_t stream, bool pdl) {
     int sb = 0;
     const int kxb = fast_yz_kxb<T>(g, &sb);
     const unsigned grid = static_cast<unsigned>((g.xh + kxb - 1) / kxb);
     switch (g.log2ly) {
 #define X(l) case l: \
-        if (g.nz == 1) k_yz<T, l, 0><<<grid, yz_threads<l>(), sb, stream>>>(S, g, tw, kt, kxb, ctl, st, prologue); \
-        else if constexpr (sizeof(T) == 4) k_yz<T, l, 1><<<grid, yz_threads<l>(), sb, stream>>>(S, g, tw, kt, kxb, ctl, st, prologue); \
+        if (g.nz == 1) launch_pdl(pdl, k_yz<T, l, 0>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue); \
+        else if constexpr (sizeof(T) == 4) launch_pdl(pdl, k_yz<T, l, 1>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue); \
         else throw std::invalid_argument("fast path: f64 needs nz == 1"); break;
         MMB_FAST_CASES(X)
 #undef X
@@ -792,13 +823,13 @@ int fast_xstep_blocks(const Geom& g) {
 template <typename T>
 void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>* tw,
                        double exch_coeff, double aniso_coeff, StepCtl* ctl, double* tpart,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, bool pdl) {
     const T coeff = static_cast<T>(exch_coeff), kan = static_cast<T>(aniso_coeff);
     switch (g.log2lx) {
 #define X(l) case l: if (xstep_small<l>(g)) { const dim3 grid((g.ny + XS<l, 16>::TR - 1) / XS<l, 16>::TR, g.nz); \
-        k_xstep<T, l, 16><<<grid, XS<l, 16>::NT, xs_smem_bytes<T, l, 16>(), stream>>>(S, m, mout, g, tw, coeff, kan, ctl, tpart); \
+        launch_pdl(pdl, k_xstep<T, l, 16>, grid, XS<l, 16>::NT, xs_smem_bytes<T, l, 16>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); \
         } else { const dim3 grid((g.ny + XS<l, 128>::TR - 1) / XS<l, 128>::TR, g.nz); \
-        k_xstep<T, l, 128><<<grid, XS<l, 128>::NT, xs_smem_bytes<T, l, 128>(), stream>>>(S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
+        launch_pdl(pdl, k_xstep<T, l, 128>, grid, XS<l, 128>::NT, xs_smem_bytes<T, l, 128>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");
@@ -814,10 +845,10 @@ void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>
                                     const StageTable&, int, cudaStream_t);                     \
     template void launch_fast_xi<T>(const cx<T>*, T*, const Geom&, const cx<T>*, cudaStream_t); \
     template void launch_fast_yz<T>(cx<T>*, const Geom&, const cx<T>*, const T*, StepCtl*,         \
-                                    const StageTable&, int, cudaStream_t);                     \
+                                    const StageTable&, int, cudaStream_t, bool);               \
     template int fast_xstep_blocks<T>(const Geom&);                                            \
     template void launch_fast_xstep<T>(cx<T>*, const T*, T*, const Geom&, const cx<T>*, double, \
-                                       double, StepCtl*, double*, cudaStream_t);
+                                       double, StepCtl*, double*, cudaStream_t, bool);
 #ifndef MMB_ONLY_F64
 MMB_FINST(float)
 #endif

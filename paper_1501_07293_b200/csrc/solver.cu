@@ -115,6 +115,7 @@ public:
         if (fast_) prepare_fast_kernels<T>(g_);
         else prepare_fft_kernels<T>(g_);
         if (fast_ && !yz_) prepare_big_kernels<T>(g_);
+        pdl_ = g.n >= (1LL << 20);
         if (const char* v = std::getenv("MMB_VERBOSE"); v && v[0] == '1')
             std::fprintf(stderr, "mmb: %dx%dx%d L=%dx%dx%d path=%s\n", d.nx, d.ny, d.nz, g.lx, g.ly, g.lz,
                          yz_ ? "yz" : (fast_ ? "big" : "general"));
@@ -155,6 +156,8 @@ public:
     ~Solver() override {
         for (auto& ge : graph_)
             if (ge) cudaGraphExecDestroy(ge);
+        for (auto& ge : batch_)
+            if (ge) cudaGraphExecDestroy(ge);
         if (ctl_host_) cudaFreeHost(ctl_host_);
         if (stream_) cudaStreamDestroy(stream_);
     }
@@ -182,6 +185,12 @@ public:
 
     void step(long long n) override {
         if (n > 0) prime();
+        // long runs replay a graph of kBatch consecutive steps (fewer graph launches)
+        for (; n >= kBatch; n -= kBatch) {
+            ensure_batch_graph(cur_);
+            ck(cudaGraphLaunch(batch_[cur_], stream_), "cudaGraphLaunch");
+            step_ += kBatch;
+        }
         for (long long i = 0; i < n; ++i) {
             ensure_graph(cur_);
             ck(cudaGraphLaunch(graph_[cur_], stream_), "cudaGraphLaunch");
@@ -297,6 +306,10 @@ public:
     float time_steps(long long n) override {
         ensure_graph(0);
         ensure_graph(1);
+        if (n >= kBatch) {
+            ensure_batch_graph(0);
+            ensure_batch_graph(1);
+        }
         cudaEvent_t a, b;
         ck(cudaEventCreate(&a), "event");
         ck(cudaEventCreate(&b), "event");
@@ -466,7 +479,7 @@ private:
             if (ev && k) ck(cudaEventRecord(ev[(*k)++], stream_), "record");
         };
         if (yz_) {
-            launch_fast_yz<T>(S_.p, g_, twy_.p, kspec_.p, ctl_.p, st_, prologue, stream_);
+            launch_fast_yz<T>(S_.p, g_, twy_.p, kspec_.p, ctl_.p, st_, prologue, stream_, pdl_);
             mark();
             return;
         }
@@ -483,7 +496,7 @@ private:
             int k = 1;
             enqueue_yz(1, &k, ev);
             launch_fast_xstep<T>(S_.p, m_[cur].p, m_[cur ^ 1].p, g_, twx_.p, exch_coeff_, aniso_coeff_,
-                                 ctl_.p, tpart_.p, stream_);
+                                 ctl_.p, tpart_.p, stream_, pdl_);
             if (ev) ck(cudaEventRecord(ev[k], stream_), "record");
             return;
         }
@@ -495,6 +508,16 @@ private:
     void enqueue_heff() {
         enqueue_demag(m_[cur_].p, hd_.p, 2);
         launch_llg<T>(1, m_[cur_].p, hd_.p, heff_.p, g_, exch_coeff_, aniso_coeff_, ctl_.p, tpart_.p, stream_);
+    }
+
+    void ensure_batch_graph(int cur) {
+        if (batch_[cur]) return;
+        cudaGraph_t gr;
+        ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+        for (int i = 0; i < kBatch; ++i) enqueue_step_eager(cur ^ (i & 1));
+        ck(cudaStreamEndCapture(stream_, &gr), "end capture");
+        ck(cudaGraphInstantiate(&batch_[cur], gr, 0), "graph instantiate");
+        cudaGraphDestroy(gr);
     }
 
     void ensure_graph(int cur) {
@@ -551,6 +574,10 @@ private:
     DevBuf<StepCtl> ctl_;
     StepCtl* ctl_host_ = nullptr;
     cudaGraphExec_t graph_[2] = {nullptr, nullptr};
+    static constexpr int kBatch = 32; // even: a batch returns M to the same buffer
+    // programmatic dependent launch between the per-step kernels: pays on large grids only
+    bool pdl_ = false;
+    cudaGraphExec_t batch_[2] = {nullptr, nullptr};
     int cur_ = 0;
     bool fast_ = false;
     bool yz_ = false;       // fast path with the fused shared-memory y/z kernel
