@@ -80,6 +80,9 @@ typedef struct mmb_stage {
 const char* mmb_status_string(int status);
 const char* mmb_last_error(void);
 const char* mmb_version(void);
+/* Frees strings returned through char** out-parameters (mmsim_string_free,
+ * proj/src/capi.cpp:102). */
+void mmb_string_free(char* s);
 
 int mmb_create(const mmb_desc* desc, const mmb_stage* stages, int nstages, mmb_ctx** out);
 void mmb_free(mmb_ctx* ctx);
@@ -116,6 +119,13 @@ int mmb_tensor_octant(mmb_ctx* ctx, double* out);
 /* Replace the device tensor with host-supplied octant entries (same layout), e.g. the
  * reference's own fp64 tensor, and rebuild the spectrum. */
 int mmb_upload_tensor_octant(mmb_ctx* ctx, const double* entries);
+
+/* Device self-check suite (mmsim_validate / run_validation, proj/src/capi.cpp:286-298,
+ * proj/src/validate.cpp:84-189, on the device): tensor invariants from the device prism-sum
+ * kernel, the spectral demag path against an O(N^2) device direct sum (up to 16^3), linearity,
+ * cube and thin-film shape factors. report_out (optional, free with mmb_string_free) receives
+ * one "PASS|FAIL  name: detail" line per check. MMB_ERROR_VALIDATION when any check fails. */
+int mmb_validate(char** report_out);
 
 /* ---- measurement ---------------------------------------------------------------------- */
 /* Device time (CUDA events on the handle's stream) of n steps, in ms. */

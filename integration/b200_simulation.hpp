@@ -6,8 +6,12 @@
 // make_simulation (proj/src/llg.cpp:163-168) then gains one branch:
 //     if (backend == Backend::b200) return std::make_unique<B200Simulation>(spec, precision);
 // after `b200` is added to `enum class Backend` (proj/include/mmsim/backend.hpp:17) and to
-// backend_from_string / to_string (proj/src/backend.cpp:10-19). Until then MMB_BACKEND_TAG
-// selects the enumerator this adapter reports.
+// backend_from_string / to_string (proj/src/backend.cpp:10-19). MMB_BACKEND_VALUE is the
+// enumerator this adapter reports (integration/b200_backend.cpp sets it to the b200 value).
+//
+// step() is synchronous, like the reference's (callers such as run_benchmark time it with a
+// wall clock); run() streams the whole batch asynchronously and synchronises only at the
+// cadence records.
 #pragma once
 
 #include <cstdint>
@@ -19,8 +23,8 @@
 #include "mmsim/errors.hpp"
 #include "mmsim/llg.hpp"
 
-#ifndef MMB_BACKEND_TAG
-#define MMB_BACKEND_TAG parallel
+#ifndef MMB_BACKEND_VALUE
+#define MMB_BACKEND_VALUE (::mmsim::Backend::parallel)
 #endif
 
 namespace mmsim {
@@ -67,7 +71,10 @@ public:
     B200Simulation(const B200Simulation&) = delete;
     B200Simulation& operator=(const B200Simulation&) = delete;
 
-    void step() override { check(mmb_step(ctx_, 1)); }
+    void step() override {
+        check(mmb_step(ctx_, 1));
+        check(mmb_synchronize(ctx_));
+    }
 
     std::int64_t run(const RunOptions& opts) override {
         long long done = 0;
@@ -102,7 +109,7 @@ public:
         return t;
     }
     const ProblemSpec& spec() const override { return spec_; }
-    Backend backend() const override { return Backend::MMB_BACKEND_TAG; }
+    Backend backend() const override { return MMB_BACKEND_VALUE; }
     Precision precision() const override { return precision_; }
 
     // Simulation<T>::magnetization() equivalents (host SoA copies).

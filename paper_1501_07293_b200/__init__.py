@@ -5,3 +5,4 @@ from .problems import (FieldSchedule, Grid, MaterialParams, ProblemSpec, Schedul
                        standard_problem_3_benchmark, standard_problem_4)
 from .simulation import (Backend, Precision, RunOptions, Simulation, TrajectoryRecord,  # noqa: F401
                          backend_from_string, make_simulation, precision_from_string)
+from .validate import ValidationReport, run_validation  # noqa: F401

@@ -18,7 +18,7 @@ EXPORTS = [
     "mmb_last_torque_sq", "mmb_run", "mmb_synchronize", "mmb_effective_field", "mmb_demag_field",
     "mmb_tensor_octant", "mmb_upload_tensor_octant", "mmb_time_steps", "mmb_profile_step",
     "mmb_launches_per_step", "mmb_device_bytes", "mmb_nccl_unique_id", "mmb_create_sharded",
-    "mmb_create_emulated", "mmb_slab",
+    "mmb_create_emulated", "mmb_slab", "mmb_validate", "mmb_string_free",
 ]
 
 
@@ -100,6 +100,9 @@ def load():
                                      C.POINTER(vp)]
     L.mmb_create_emulated.argtypes = [C.POINTER(MmbDesc), C.POINTER(MmbStage), i, i, C.POINTER(vp)]
     L.mmb_slab.argtypes = [vp, C.POINTER(i), C.POINTER(i)]
+    L.mmb_validate.argtypes = [C.POINTER(C.c_void_p)]
+    L.mmb_string_free.argtypes = [C.c_void_p]
+    L.mmb_string_free.restype = None
     _lib = L
     return L
 

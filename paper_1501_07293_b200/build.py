@@ -58,6 +58,7 @@ UNITS = [
     ("tensor.o", "tensor_kernels.cu", ["--fmad=false"]),
     ("solver.o", "solver.cu", []),
     ("shard.o", "shard.cu", []),
+    ("validate.o", "validate.cu", []),
 ]
 
 

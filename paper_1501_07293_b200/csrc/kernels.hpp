@@ -60,6 +60,8 @@ int reduce_blocks(long long n);
 // K0: fp64 prism-sum entries on the non-negative octant, E[6][nz][ny][nx]
 // (proj/src/demag_tensor.cpp:9-43).
 void launch_tensor_octant(double* E, int nx, int ny, int nz, double delta, cudaStream_t stream);
+// The same prism sums at n signed offsets ijk[3n] -> out[6n] (validation suite).
+void launch_tensor_entries(const int* ijk, int n, double delta, double* out, cudaStream_t stream);
 // Per-axis real cosine / sine transform of the octant (wrapped-kernel spectrum), fp64.
 // in dims (d0 fastest, d1, d2); transforms axis `axis` from length n to L/2+1 (1 if L == 1).
 void launch_axis_transform(const double* in, double* out, int d0, int d1, int d2, int axis,

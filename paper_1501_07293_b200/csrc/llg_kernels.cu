@@ -265,15 +265,9 @@ __global__ void __launch_bounds__(kRedThreads) k_energy(const T* __restrict__ m,
     }
 }
 
-// K0: the eight-corner prism sums (proj/src/demag_tensor.cpp:9-43) in fp64 for offsets
-// (I, J, K) >= 0; other octants follow by parity. E is [6][nz][ny][nx].
-__global__ void k_tensor_octant(double* __restrict__ E, int nx, int ny, int nz, double delta) {
-    const long long cnt = static_cast<long long>(nx) * ny * nz;
-    const long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (f >= cnt) return;
-    const int I = static_cast<int>(f % nx);
-    const int J = static_cast<int>((f / nx) % ny);
-    const int K = static_cast<int>(f / (static_cast<long long>(nx) * ny));
+// The eight-corner prism sums (proj/src/demag_tensor.cpp:9-43) in fp64 at integer offset
+// (I, J, K) of any sign, in the order xx, xy, xz, yy, yz, zz.
+__device__ __forceinline__ void tensor_entry(int I, int J, int K, double delta, double e[6]) {
     double xx = 0, xy = 0, xz = 0, yy = 0, yz = 0, zz = 0;
 #pragma unroll
     for (int i = 0; i <= 1; ++i)
@@ -294,12 +288,37 @@ __global__ void k_tensor_octant(double* __restrict__ E, int nx, int ny, int nz, 
                 yz += sign * log(x * delta + r);
             }
     const double p = 1.0 / (4.0 * 3.14159265358979323846);
-    E[0 * cnt + f] = xx * p;
-    E[1 * cnt + f] = xy * -p;
-    E[2 * cnt + f] = xz * -p;
-    E[3 * cnt + f] = yy * p;
-    E[4 * cnt + f] = yz * -p;
-    E[5 * cnt + f] = zz * p;
+    e[0] = xx * p;
+    e[1] = xy * -p;
+    e[2] = xz * -p;
+    e[3] = yy * p;
+    e[4] = yz * -p;
+    e[5] = zz * p;
+}
+
+// K0: tensor_entry on the non-negative octant; other octants follow by parity.
+// E is [6][nz][ny][nx].
+__global__ void k_tensor_octant(double* __restrict__ E, int nx, int ny, int nz, double delta) {
+    const long long cnt = static_cast<long long>(nx) * ny * nz;
+    const long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (f >= cnt) return;
+    const int I = static_cast<int>(f % nx);
+    const int J = static_cast<int>((f / nx) % ny);
+    const int K = static_cast<int>(f / (static_cast<long long>(nx) * ny));
+    double e[6];
+    tensor_entry(I, J, K, delta, e);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) E[c * cnt + f] = e[c];
+}
+
+// tensor_entry at n arbitrary offsets ijk[3n] -> out[6n] (validation suite).
+__global__ void k_tensor_entries(const int* __restrict__ ijk, int n, double delta, double* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double e[6];
+    tensor_entry(ijk[3 * t], ijk[3 * t + 1], ijk[3 * t + 2], delta, e);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) out[6 * t + c] = e[c];
 }
 
 } // namespace
@@ -351,6 +370,12 @@ void launch_energy(const T* m, const T* hd, const Geom& g, double ku_over_ms2, c
     const int nb = reduce_blocks(g.n);
     k_energy<T><<<nb, kRedThreads, 0, stream>>>(m, hd, g, ku_over_ms2, ctl, partial);
     k_final_sum<2><<<1, 64, 0, stream>>>(partial, nb, out);
+    check_launch();
+}
+
+void launch_tensor_entries(const int* ijk, int n, double delta, double* out, cudaStream_t stream) {
+    if (n <= 0) return;
+    k_tensor_entries<<<(n + 127) / 128, 128, 0, stream>>>(ijk, n, delta, out);
     check_launch();
 }
 

@@ -22,6 +22,7 @@
 #include "fast.hpp"
 #include "kernels.hpp"
 #include "solver_base.hpp"
+#include "validate.hpp"
 
 namespace mmb {
 
@@ -648,6 +649,25 @@ const char* mmb_status_string(int status) {
 }
 
 const char* mmb_last_error(void) { return t_last_error.c_str(); }
+
+void mmb_string_free(char* s) { delete[] s; }
+
+int mmb_validate(char** report_out) {
+    return guarded([&] {
+        bool ok = false;
+        const std::string report = mmb::run_device_validation(ok);
+        if (report_out) {
+            char* out = new char[report.size() + 1];
+            std::memcpy(out, report.c_str(), report.size() + 1);
+            *report_out = out;
+        }
+        if (!ok) {
+            t_last_error = "validation suite reported failing checks";
+            return static_cast<int>(MMB_ERROR_VALIDATION);
+        }
+        return static_cast<int>(MMB_OK);
+    });
+}
 const char* mmb_version(void) { return "0.1.0-b200"; }
 
 int mmb_create(const mmb_desc* desc, const mmb_stage* stages, int nstages, mmb_ctx** out) {

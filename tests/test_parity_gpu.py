@@ -282,6 +282,32 @@ def test_512x512x8_f32_properties(path):
     assert rel(sim.demag_field(m1), want) <= 1e-5
 
 
+def test_device_validation_suite():
+    """mmb_validate: the reference's validate checks on the device (SURVEY.md §8(f) #4)."""
+    from paper_1501_07293_b200 import run_validation
+    rep = run_validation()
+    assert rep.passed, rep.text
+    names = [ln.split(":")[0][6:] for ln in rep.lines[:-1]]
+    for want in ["tensor trace at zero offset (+1)", "tensor parity symmetry", "tensor permutation symmetry",
+                 "fft-vs-direct f64 8x8x4", "fft-vs-direct f32 8x8x4", "fft-vs-direct f64 16x16x16",
+                 "fft linearity", "cube shape factor (avg Hx vs -ms/3)", "thin-film central demag factor"]:
+        assert want in names, rep.text
+    assert rep.lines[-1] == "all checks passed"
+
+
+def test_mmsim_c_api_with_b200_backend(tmp_path):
+    """The reference's own C API (mmsim.h) with `backend = b200` selected in the config: sim
+    handle calls, mmsim_simulate's trajectory file and mmsim_benchmark's table against the
+    reference's serial backend (integration/mmsim_b200_check.c, prebuilt by the CPU suite)."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(HERE), "build", "integration", "mmsim_b200_check")
+    if not os.path.exists(exe):
+        pytest.skip("integration not built (CPU suite builds it where /root/reference exists)")
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "mmsim b200 check: ok" in r.stdout
+
+
 def test_reference_side_adapter_runs():
     """The SimulationBase adapter (integration/b200_simulation.hpp), prebuilt here by the CPU
     suite, drives the B200 path through the C-ABI: 10 steps, 2 cadence records."""
