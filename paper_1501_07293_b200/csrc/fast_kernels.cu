@@ -698,6 +698,10 @@ void set_smem(K kernel, int bytes) {
     }
 }
 
+#ifndef MMB_XS_PB
+#define MMB_XS_PB 128 // KXS tile: 3 * (PB / N2) row pairs (XS)
+#endif
+
 #define MMB_FAST_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12)
 
 } // namespace
@@ -743,7 +747,7 @@ template <typename T>
 void prepare_fast_kernels(const Geom& g) {
     switch (g.log2lx) {
 #define X(l) case l: set_smem(k_xf<T, l>, x_smem_bytes<T, l>()); set_smem(k_xi<T, l>, x_smem_bytes<T, l>()); \
-                     set_smem(k_xstep<T, l, 128>, xs_smem_bytes<T, l, 128>()); \
+                     set_smem(k_xstep<T, l, MMB_XS_PB>, xs_smem_bytes<T, l, MMB_XS_PB>()); \
                      set_smem(k_xstep<T, l, 16>, xs_smem_bytes<T, l, 16>()); break;
         MMB_FAST_CASES(X)
 #undef X
@@ -806,14 +810,14 @@ void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, StepC
 
 template <int LOG2L>
 bool xstep_small(const Geom& g) {
-    return ((g.ny + XS<LOG2L, 128>::TR - 1) / XS<LOG2L, 128>::TR) * g.nz < 2 * 148;
+    return ((g.ny + XS<LOG2L, MMB_XS_PB>::TR - 1) / XS<LOG2L, MMB_XS_PB>::TR) * g.nz < 2 * 148;
 }
 
 template <typename T>
 int fast_xstep_blocks(const Geom& g) {
     switch (g.log2lx) {
 #define X(l) case l: return xstep_small<l>(g) ? ((g.ny + XS<l, 16>::TR - 1) / XS<l, 16>::TR) * g.nz \
-                                              : ((g.ny + XS<l, 128>::TR - 1) / XS<l, 128>::TR) * g.nz;
+                                              : ((g.ny + XS<l, MMB_XS_PB>::TR - 1) / XS<l, MMB_XS_PB>::TR) * g.nz;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");
@@ -828,8 +832,8 @@ void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>
     switch (g.log2lx) {
 #define X(l) case l: if (xstep_small<l>(g)) { const dim3 grid((g.ny + XS<l, 16>::TR - 1) / XS<l, 16>::TR, g.nz); \
         launch_pdl(pdl, k_xstep<T, l, 16>, grid, XS<l, 16>::NT, xs_smem_bytes<T, l, 16>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); \
-        } else { const dim3 grid((g.ny + XS<l, 128>::TR - 1) / XS<l, 128>::TR, g.nz); \
-        launch_pdl(pdl, k_xstep<T, l, 128>, grid, XS<l, 128>::NT, xs_smem_bytes<T, l, 128>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
+        } else { const dim3 grid((g.ny + XS<l, MMB_XS_PB>::TR - 1) / XS<l, MMB_XS_PB>::TR, g.nz); \
+        launch_pdl(pdl, k_xstep<T, l, MMB_XS_PB>, grid, XS<l, MMB_XS_PB>::NT, xs_smem_bytes<T, l, MMB_XS_PB>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");
