@@ -24,11 +24,13 @@ void check_launch() {
     if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch: ") + cudaGetErrorString(e));
 }
 
+// Rows per CTA: enough that stage A (the larger register DFT, P*N1 tasks) has a task for
+// every thread; stage B (P*N2 tasks) loops when N2 > N1.
 template <int LOG2L>
 struct YR {
     using SP = Split<LOG2L>;
-    static constexpr int P = SP::N2 >= 256 ? 1 : 256 / SP::N2; // rows per CTA
-    static constexpr int NT = P * SP::N2;
+    static constexpr int NT = SP::N2 >= 256 ? SP::N2 : 256;
+    static constexpr int P = NT / SP::N1 > 0 ? NT / SP::N1 : 1;
     static constexpr int EX = SP::N1 + 1;
 };
 template <typename T, int LOG2L>
@@ -54,8 +56,9 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
     __syncthreads();
     const int tid = threadIdx.x;
     const long long r0 = static_cast<long long>(blockIdx.x) * P;
-    if (tid < P * N1) {
-        const int p = tid / N1, n1 = tid % N1;
+    constexpr int NT = YR<LOG2L>::NT;
+    for (int ta = tid; ta < P * N1; ta += NT) {
+        const int p = ta / N1, n1 = ta % N1;
         const long long r = r0 + p;
         cx<T> v[N2];
         if (r < nrows) {
@@ -86,8 +89,8 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
         }
     }
     __syncthreads();
-    {
-        const int p = tid / N2, k2 = tid % N2;
+    for (int tb = tid; tb < P * N2; tb += NT) {
+        const int p = tb / N2, k2 = tb % N2;
         const long long r = r0 + p;
         if (r < nrows) {
             cx<T> u[N1];

@@ -423,9 +423,14 @@ struct XS {
     using SP = Split<LOG2L>;
     // Lx = 4096 halves the tile so exchange buffer + twiddle table stay within 227 KB
     static constexpr int PBE = (LOG2L >= 12 && PB > 16) ? PB / 2 : PB;
-    static constexpr int P = 3 * (SP::N2 >= PBE ? 1 : PBE / SP::N2);  // row pairs
+    // WIDE (Lx = 2048: N2 = 2 N1): one stage-A task (the DFT_N2 in registers) per thread and
+    // stage B in RB = N2 / N1 rounds, so the register-heavy stage keeps every warp busy
+    static constexpr bool WIDE = LOG2L == 11 && PB > 16;
+    static constexpr int RB = WIDE ? SP::N2 / SP::N1 : 1;
+    static constexpr int P = WIDE ? 3 * (PBE / SP::N1)                 // row pairs
+                                  : 3 * (SP::N2 >= PBE ? 1 : PBE / SP::N2);
     static constexpr int TR = 2 * P / 3;                              // y rows per CTA
-    static constexpr int NT = P * SP::N2;                             // threads
+    static constexpr int NT = WIDE ? P * SP::N1 : P * SP::N2;         // threads
     static constexpr int XHP = ((1 << LOG2L) / 2 + 1) | 1;            // staging pitch (odd)
     static constexpr int EX = SP::N1 + 1;
     static constexpr int ZP = (1 << LOG2L) + 1;
@@ -524,9 +529,13 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
         }
     }
     __syncthreads();
-    // ---- 1c. inverse stage B -> H_demag tile (the nx live cells)
-    {
-        const int pb = tid / N2, k2 = tid % N2;
+    // ---- 1c. inverse stage B -> H_demag tile (the nx live cells). With RB = 2 rounds, the
+    // tile rows of round r lie inside exchange rows already consumed (round 0: its own,
+    // synchronised below; round 1: round 0's), never in round 1's.
+#pragma unroll 1
+    for (int rnd = 0; rnd < X::RB; ++rnd) {
+        const int tb = tid + rnd * NT;
+        const int pb = tb / N2, k2 = tb % N2;
         cx<T> u[N1];
         const cx<T>* ex = sm + (pb * N2 + k2) * EX;
 #pragma unroll
@@ -624,9 +633,11 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
         }
     }
     __syncthreads();
-    // ---- 3b. forward stage B -> natural-order Z rows
-    {
-        const int pb = tid / N2, k2 = tid % N2;
+    // ---- 3b. forward stage B -> natural-order Z rows (RB rounds, as in 1c)
+#pragma unroll 1
+    for (int rnd = 0; rnd < X::RB; ++rnd) {
+        const int tb = tid + rnd * NT;
+        const int pb = tb / N2, k2 = tb % N2;
         cx<T> u[N1];
         const cx<T>* ex = sm + (pb * N2 + k2) * EX;
 #pragma unroll
@@ -747,7 +758,7 @@ template <typename T>
 void prepare_fast_kernels(const Geom& g) {
     switch (g.log2lx) {
 #define X(l) case l: set_smem(k_xf<T, l>, x_smem_bytes<T, l>()); set_smem(k_xi<T, l>, x_smem_bytes<T, l>()); \
-                     set_smem(k_xstep<T, l, MMB_XS_PB>, xs_smem_bytes<T, l, MMB_XS_PB>()); \
+                     if (xs_smem_bytes<T, l, MMB_XS_PB>() <= 227 * 1024) set_smem(k_xstep<T, l, MMB_XS_PB>, xs_smem_bytes<T, l, MMB_XS_PB>()); \
                      set_smem(k_xstep<T, l, 16>, xs_smem_bytes<T, l, 16>()); break;
         MMB_FAST_CASES(X)
 #undef X
@@ -832,7 +843,8 @@ void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>
     switch (g.log2lx) {
 #define X(l) case l: if (xstep_small<l>(g)) { const dim3 grid((g.ny + XS<l, 16>::TR - 1) / XS<l, 16>::TR, g.nz); \
         launch_pdl(pdl, k_xstep<T, l, 16>, grid, XS<l, 16>::NT, xs_smem_bytes<T, l, 16>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); \
-        } else { const dim3 grid((g.ny + XS<l, MMB_XS_PB>::TR - 1) / XS<l, MMB_XS_PB>::TR, g.nz); \
+        } else { if (xs_smem_bytes<T, l, MMB_XS_PB>() > 227 * 1024) throw std::invalid_argument("fast path: x tile exceeds shared memory"); \
+        const dim3 grid((g.ny + XS<l, MMB_XS_PB>::TR - 1) / XS<l, MMB_XS_PB>::TR, g.nz); \
         launch_pdl(pdl, k_xstep<T, l, MMB_XS_PB>, grid, XS<l, MMB_XS_PB>::NT, xs_smem_bytes<T, l, MMB_XS_PB>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
         MMB_FAST_CASES(X)
 #undef X

@@ -308,6 +308,29 @@ def test_mmsim_c_api_with_b200_backend(tmp_path):
     assert "mmsim b200 check: ok" in r.stdout
 
 
+@pytest.mark.parametrize("grid", [(600, 400, 6, 1.0), (1024, 300, 12, 1.0)])
+def test_wide_x_tile_steps_match_general_path(grid, monkeypatch):
+    """Lx = 2048 x-tiles (XS::WIDE: one DFT_64 task per thread, stage B in two rounds) on grids
+    large enough to take the 8-row tile, on the fused y/z path and on the streaming y/z path
+    (nz > 8): 3 steps against the unfused general pipeline, itself checked against the
+    reference on the small grids above."""
+    nx, ny, nz, delta = grid
+    sp = spec(nx, ny, nz, delta, 1e7, 1000.0, 100.0, 0.5, 1e-5)
+    rng = np.random.default_rng(3)
+    v = rng.uniform(-1, 1, (3, nz, ny, nx))
+    m0 = (1000.0 * v / np.sqrt((v * v).sum(0))).astype(np.float32)
+    out = {}
+    for name in ("fast", "general"):
+        monkeypatch.delenv("MMB_GENERAL_PATH", raising=False)
+        if name == "general":
+            monkeypatch.setenv("MMB_GENERAL_PATH", "1")
+        sim = b200(sp, "f32")
+        sim.set_magnetization(m0)
+        sim.step(3)
+        out[name] = sim.magnetization()
+    assert rel(out["fast"], out["general"].astype(np.float64)) <= 1e-5
+
+
 def test_reference_side_adapter_runs():
     """The SimulationBase adapter (integration/b200_simulation.hpp), prebuilt here by the CPU
     suite, drives the B200 path through the C-ABI: 10 steps, 2 cadence records."""
