@@ -52,7 +52,7 @@ UNITS = [
     ("fft_f64.o", "fft_kernels.cu", ["-DMMB_ONLY_F64"]),
     ("fast_f32.o", "fast_kernels.cu", ["-DMMB_ONLY_F32"] + os.environ.get("MMB_XFLAGS", "").split()),
     ("fast_f64.o", "fast_kernels.cu", ["-DMMB_ONLY_F64"]),
-    ("big_f32.o", "big_kernels.cu", ["-DMMB_ONLY_F32"]),
+    ("big_f32.o", "big_kernels.cu", ["-DMMB_ONLY_F32"] + os.environ.get("MMB_XFLAGS", "").split()),
     ("big_f64.o", "big_kernels.cu", ["-DMMB_ONLY_F64"]),
     ("llg.o", "llg_kernels.cu", ["--fmad=false"]),
     ("tensor.o", "tensor_kernels.cu", ["--fmad=false"]),

@@ -116,8 +116,11 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
 }
 
 // z pencils: W consecutive ky of one kx, all three components, Lz = 2^LOG2LZ >= 2 nz - 1.
+#ifndef MMB_ZW32
+#define MMB_ZW32 32
+#endif
 template <typename T>
-constexpr int zw() { return sizeof(T) == 4 ? 32 : 16; }
+constexpr int zw() { return sizeof(T) == 4 ? MMB_ZW32 : 16; }
 constexpr int kZThreads = 256;
 template <typename T, int LOG2LZ>
 constexpr int z_smem_bytes() {
@@ -178,9 +181,23 @@ __global__ void __launch_bounds__(kZThreads)
     }
     __syncthreads();
 
-    // fused middle: task (k2, w)
+    // fused middle: task (k2, w). The task's N1 tensor coefficient sets are loaded first, so
+    // their global latency overlaps the forward DFTs.
     for (int t = tid; t < N2 * W; t += kZThreads) {
         const int w = t % W, k2 = t / W;
+        const int ky = ky0 + w;
+        const bool fy = 2 * ky > ly;
+        const int kyo = fy ? ly - ky : ky;
+        const T* kb = kt + (static_cast<long long>(kx) * zh * yh + kyo) * 6;
+        T k6[N1][6];
+        if (w < wl) {
+#pragma unroll
+            for (int k1 = 0; k1 < N1; ++k1) {
+                const int kz = k2 + N2 * k1;
+                const int kzo = 2 * kz > LZ ? LZ - kz : kz;
+                load6<T>(kb + static_cast<long long>(kzo) * yh * 6, k6[k1]);
+            }
+        }
         cx<T> u[3][N1];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -190,21 +207,14 @@ __global__ void __launch_bounds__(kZThreads)
             DftP<N1, -1, N1, N1>::run(u[c]);
         }
         if (w < wl) {
-            const int ky = ky0 + w;
-            const bool fy = 2 * ky > ly;
-            const int kyo = fy ? ly - ky : ky;
-            const T* kb = kt + (static_cast<long long>(kx) * zh * yh + kyo) * 6;
 #pragma unroll
             for (int k1 = 0; k1 < N1; ++k1) {
                 const int kz = k2 + N2 * k1;
                 const bool fz = 2 * kz > LZ;
-                const int kzo = fz ? LZ - kz : kz;
-                T k6[6];
-                load6<T>(kb + static_cast<long long>(kzo) * yh * 6, k6);
-                if (fy) k6[1] = -k6[1];
-                if (fz) k6[2] = -k6[2];
-                if (fy != fz) k6[4] = -k6[4];
-                mac3<T>(k6, u[0][k1], u[1][k1], u[2][k1]);
+                if (fy) k6[k1][1] = -k6[k1][1];
+                if (fz) k6[k1][2] = -k6[k1][2];
+                if (fy != fz) k6[k1][4] = -k6[k1][4];
+                mac3<T>(k6[k1], u[0][k1], u[1][k1], u[2][k1]);
             }
         }
 #pragma unroll
