@@ -24,14 +24,17 @@ void check_launch() {
     if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch: ") + cudaGetErrorString(e));
 }
 
-// Rows per CTA: enough that stage A (the larger register DFT, P*N1 tasks) has a task for
-// every thread; stage B (P*N2 tasks) loops when N2 > N1.
+// Rows per CTA: every thread has exactly one stage-A task. DFT_64 stages run on lane pairs
+// (dft_pair: 32 values per lane instead of 64), so LA / LB lanes share a stage-A / stage-B
+// task; stage B loops when it has more tasks than threads.
 template <int LOG2L>
 struct YR {
     using SP = Split<LOG2L>;
-    static constexpr int NT = SP::N2 >= 256 ? SP::N2 : 256;
-    static constexpr int P = NT / SP::N1 > 0 ? NT / SP::N1 : 1;
+    static constexpr int LA = SP::N2 == 64 ? 2 : 1, LB = SP::N1 == 64 ? 2 : 1;
+    static constexpr int NT = 256;
+    static constexpr int P = NT / (SP::N1 * LA);
     static constexpr int EX = SP::N1 + 1;
+    static_assert(P >= 1 && P * SP::N1 * LA == NT, "row tile");
 };
 template <typename T, int LOG2L>
 constexpr int yr_smem_bytes() {
@@ -47,7 +50,10 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
            int out_pitch, int n_live, const cx<T>* __restrict__ tw, StepCtl* ctl, StageTable st,
            int prologue) {
     using SP = Split<LOG2L>;
-    constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = YR<LOG2L>::P, EX = YR<LOG2L>::EX;
+    using Y = YR<LOG2L>;
+    constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = Y::P, EX = Y::EX, NT = Y::NT;
+    constexpr int LA = Y::LA, LB = Y::LB, RA = N2 / LA, RB = N1 / LB;
+    constexpr int SIGN = INV ? +1 : -1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
     cx<T>* tws = sm + P * N2 * EX;
@@ -56,59 +62,57 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
     __syncthreads();
     const int tid = threadIdx.x;
     const long long r0 = static_cast<long long>(blockIdx.x) * P;
-    constexpr int NT = YR<LOG2L>::NT;
-    for (int ta = tid; ta < P * N1; ta += NT) {
-        const int p = ta / N1, n1 = ta % N1;
+    {
+        // stage A: lane h of the task takes n2 = LA m + h
+        const int h = LA == 2 ? (tid & 1) : 0, task = LA == 2 ? (tid >> 1) : tid;
+        const int p = task / N1, n1 = task % N1;
         const long long r = r0 + p;
-        cx<T> v[N2];
+        cx<T> v[RA];
+        constexpr int NZ = INV ? RA : (RA / 2 > 0 ? RA / 2 : 1); // forward: n2 < N2 / 2 live
+#pragma unroll
+        for (int m = 0; m < RA; ++m) v[m] = cx<T>{0, 0};
         if (r < nrows) {
             const cx<T>* src = in + r * in_pitch;
-            if constexpr (!INV) {
-                constexpr int NZ = N2 / 2;
 #pragma unroll
-                for (int n2 = 0; n2 < NZ; ++n2) {
-                    const int y = n1 + N1 * n2;
-                    v[n2] = y < n_live ? src[y] : cx<T>{0, 0};
-                }
-                DftP<N2, -1, NZ, N2>::run(v);
-            } else {
-#pragma unroll
-                for (int n2 = 0; n2 < N2; ++n2) v[n2] = src[n1 + N1 * n2];
-                DftP<N2, +1, N2, N2>::run(v);
+            for (int m = 0; m < NZ; ++m) {
+                const int y = n1 + N1 * (LA * m + h);
+                v[m] = (INV || y < n_live) ? src[y] : cx<T>{0, 0};
             }
-        } else {
-#pragma unroll
-            for (int n2 = 0; n2 < N2; ++n2) v[n2] = cx<T>{0, 0};
         }
+        if constexpr (LA == 2) dft_pair<RA, SIGN, NZ>(v, h);
+        else DftP<N2, SIGN, NZ, N2>::run(v);
         cx<T>* ex = sm + (p * N2) * EX + n1;
 #pragma unroll
-        for (int k2 = 0; k2 < N2; ++k2) {
-            cx<T> w = v[k2];
+        for (int kk = 0; kk < RA; ++kk) {
+            const int k2 = kk + RA * h;
+            cx<T> w = v[kk];
             if (k2 > 0) w = INV ? cmulc(w, tws[k2 * N1 + n1]) : cmul(w, tws[k2 * N1 + n1]);
             ex[k2 * EX] = w;
         }
     }
     __syncthreads();
-    for (int tb = tid; tb < P * N2; tb += NT) {
-        const int p = tb / N2, k2 = tb % N2;
+    // stage B: lane h of the task takes n1 = LB q + h; rows past nrows compute on zeros and
+    // skip only their stores (the pair shuffles need every lane)
+    for (int tb = tid; tb < P * N2 * LB; tb += NT) {
+        const int h = LB == 2 ? (tb & 1) : 0, task = LB == 2 ? (tb >> 1) : tb;
+        const int p = task / N2, k2 = task % N2;
         const long long r = r0 + p;
+        cx<T> u[RB];
+        const cx<T>* ex = sm + (p * N2 + k2) * EX + h;
+#pragma unroll
+        for (int q = 0; q < RB; ++q) u[q] = ex[LB * q];
+        if constexpr (LB == 2) dft_pair<RB, SIGN, RB>(u, h);
+        else DftP<N1, SIGN, N1, (INV && N1 > 1) ? N1 / 2 : N1>::run(u);
         if (r < nrows) {
-            cx<T> u[N1];
-            const cx<T>* ex = sm + (p * N2 + k2) * EX;
-#pragma unroll
-            for (int q = 0; q < N1; ++q) u[q] = ex[q];
             cx<T>* dst = out + r * out_pitch;
-            if constexpr (!INV) {
-                DftP<N1, -1, N1, N1>::run(u);
 #pragma unroll
-                for (int k1 = 0; k1 < N1; ++k1) dst[k2 + N2 * k1] = u[k1];
-            } else {
-                constexpr int NO = N1 == 1 ? 1 : N1 / 2;
-                DftP<N1, +1, N1, NO>::run(u);
-#pragma unroll
-                for (int k1 = 0; k1 < NO; ++k1) {
-                    const int y = k2 + N2 * k1;
-                    if (y < n_live) dst[y] = u[k1];
+            for (int q = 0; q < RB; ++q) {
+                const int k1 = q + RB * h;
+                const int y = k2 + N2 * k1;
+                if (!INV) {
+                    dst[y] = u[q];
+                } else if (k1 < (N1 > 1 ? N1 / 2 : 1) && y < n_live) {
+                    dst[y] = u[q];
                 }
             }
         }
