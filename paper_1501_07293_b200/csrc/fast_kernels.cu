@@ -423,14 +423,20 @@ struct XS {
     using SP = Split<LOG2L>;
     // Lx = 4096 halves the tile so exchange buffer + twiddle table stay within 227 KB
     static constexpr int PBE = (LOG2L >= 12 && PB > 16) ? PB / 2 : PB;
-    // WIDE (Lx = 2048: N2 = 2 N1): one stage-A task (the DFT_N2 in registers) per thread and
-    // stage B in RB = N2 / N1 rounds, so the register-heavy stage keeps every warp busy
+    // Lx = 2048 (N2 = 64 = 2 N1), WIDE: one stage-A task (DFT_64 in registers) per thread, 3 x 8
+    // rows per CTA, stage B in RB = 2 rounds. Lx = 4096 (N1 = N2 = 64), PAIR: every DFT_64
+    // task runs on a lane pair (dft_pair, 32 values per lane); LA / LB = lanes per stage-A /
+    // stage-B task. (PAIR at Lx = 2048 with 3 x 2 rows and 3 CTAs/SM measured 26 % slower than
+    // WIDE: the narrow tiles re-read more neighbour rows.)
     static constexpr bool WIDE = LOG2L == 11 && PB > 16;
+    static constexpr bool PAIR = LOG2L >= 11 && !WIDE;
+    static constexpr int LA = PAIR ? 2 : 1, LB = (PAIR && SP::N1 == 64) ? 2 : 1;
     static constexpr int RB = WIDE ? SP::N2 / SP::N1 : 1;
-    static constexpr int P = WIDE ? 3 * (PBE / SP::N1)                 // row pairs
-                                  : 3 * (SP::N2 >= PBE ? 1 : PBE / SP::N2);
-    static constexpr int TR = 2 * P / 3;                              // y rows per CTA
-    static constexpr int NT = WIDE ? P * SP::N1 : P * SP::N2;         // threads
+    static constexpr int P = PAIR ? 3
+                                  : (WIDE ? 3 * (PBE / SP::N1) : 3 * (SP::N2 >= PBE ? 1 : PBE / SP::N2));
+    static constexpr int TR = 2 * P / 3;                                        // y rows per CTA
+    static constexpr int NT = WIDE ? P * SP::N1 : P * SP::N2 * LB;              // threads
+    static_assert(P * SP::N1 * LA <= NT && P * SP::N2 * LB == NT * RB, "stage tasks");
     static constexpr int XHP = ((1 << LOG2L) / 2 + 1) | 1;            // staging pitch (odd)
     static constexpr int EX = SP::N1 + 1;
     static constexpr int ZP = (1 << LOG2L) + 1;
@@ -444,8 +450,9 @@ constexpr int xs_smem_bytes() {
 
 template <typename T, int LOG2L, int PB>
 constexpr int xs_min_blocks() {
-    // two CTAs per SM when their shared memory fits (registers capped accordingly)
-    return 2 * xs_smem_bytes<T, LOG2L, PB>() + 4096 <= 228 * 1024 ? 2 : 1;
+    // two or three CTAs per SM when their shared memory fits (registers capped accordingly)
+    constexpr int b = xs_smem_bytes<T, LOG2L, PB>() + 2048;
+    return (XS<LOG2L, PB>::NT <= 256 && 3 * b <= 228 * 1024) ? 3 : (2 * b <= 228 * 1024 ? 2 : 1);
 }
 
 // PB = 128: ~384 threads and 3 x 8 rows per CTA (large grids); PB = 16: 3 x 2 rows for
@@ -494,16 +501,19 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
     cp_async_wait_all();
     __syncthreads();
 
-    // ---- 1b. inverse stage A on Z = A + iB (rows 2p, 2p+1 of the same component)
-    cx<T> v[N2];
-    const bool a_task = tid < P * N1;
-    const int pa = tid / N1, n1 = tid % N1;
+    // ---- 1b. inverse stage A on Z = A + iB (rows 2p, 2p+1 of the same component); lane
+    // h of a pair task takes n2 = LA m + h
+    constexpr int LA = X::LA, LB = X::LB, RA = N2 / LA, RBq = N1 / LB;
+    cx<T> v[RA];
+    const int ha = LA == 2 ? (tid & 1) : 0, ta = LA == 2 ? (tid >> 1) : tid;
+    const bool a_task = ta < P * N1;
+    const int pa = ta / N1, n1 = ta % N1;
     if (a_task) {
         const cx<T>* A = sm + (2 * pa) * XHP;
         const cx<T>* B = A + XHP;
 #pragma unroll
-        for (int n2 = 0; n2 < N2; ++n2) {
-            const int k = n1 + N1 * n2;
+        for (int m = 0; m < RA; ++m) {
+            const int k = n1 + N1 * (LA * m + ha);
             cx<T> zv;
             if (k == 0 || 2 * k == L) {
                 zv = cx<T>{A[k].x, B[k].x};
@@ -514,43 +524,49 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
                 const cx<T> a = A[L - k], b = B[L - k];
                 zv = cx<T>{a.x + b.y, b.x - a.y};
             }
-            v[n2] = zv;
+            v[m] = zv;
         }
-        DftP<N2, +1, N2, N2>::run(v);
+        if constexpr (LA == 2) dft_pair<RA, +1, RA>(v, ha);
+        else DftP<N2, +1, N2, N2>::run(v);
     }
     __syncthreads();
     if (a_task) {
         cx<T>* ex = sm + (pa * N2) * EX + n1;
 #pragma unroll
-        for (int k2 = 0; k2 < N2; ++k2) {
-            cx<T> w = v[k2];
+        for (int kk = 0; kk < RA; ++kk) {
+            const int k2 = kk + RA * ha;
+            cx<T> w = v[kk];
             if (k2 > 0) w = cmulc(w, tws[k2 * N1 + n1]);
             ex[k2 * EX] = w;
         }
     }
     __syncthreads();
-    // ---- 1c. inverse stage B -> H_demag tile (the nx live cells). With RB = 2 rounds, the
-    // tile rows of round r lie inside exchange rows already consumed (round 0: its own,
-    // synchronised below; round 1: round 0's), never in round 1's.
+    // ---- 1c. inverse stage B -> H_demag tile (the nx live cells); lane h of a pair task
+    // takes n1 = LB q + h and returns k1 = q + RBq h
+    const int hb_ = LB == 2 ? (tid & 1) : 0, tb0 = LB == 2 ? (tid >> 1) : tid;
+    // RB = 2 (WIDE): the tile rows of round r lie inside exchange rows already consumed
+    // (round 0: its own, synchronised below; round 1: round 0's), never in round 1's
 #pragma unroll 1
     for (int rnd = 0; rnd < X::RB; ++rnd) {
-        const int tb = tid + rnd * NT;
-        const int pb = tb / N2, k2 = tb % N2;
-        cx<T> u[N1];
-        const cx<T>* ex = sm + (pb * N2 + k2) * EX;
+        const int tb = tb0 + rnd * NT;
+        const int pb = tb / N2, k2b = tb % N2;
+        cx<T> u[RBq];
+        const cx<T>* ex = sm + (pb * N2 + k2b) * EX + hb_;
 #pragma unroll
-        for (int q = 0; q < N1; ++q) u[q] = ex[q];
+        for (int q = 0; q < RBq; ++q) u[q] = ex[LB * q];
         constexpr int NO = N1 == 1 ? 1 : N1 / 2;
-        DftP<N1, +1, N1, NO>::run(u);
+        if constexpr (LB == 2) dft_pair<RBq, +1, RBq>(u, hb_);
+        else DftP<N1, +1, N1, NO>::run(u);
         __syncthreads(); // the tile overlays the exchange buffer
-        T* ha = hm + (2 * pb) * nx;
-        T* hb = ha + nx;
+        T* ha_row = hm + (2 * pb) * nx;
+        T* hb_row = ha_row + nx;
 #pragma unroll
-        for (int k1 = 0; k1 < NO; ++k1) {
-            const int x = k2 + N2 * k1;
-            if (x < nx) {
-                ha[x] = u[k1].x;
-                hb[x] = u[k1].y;
+        for (int q = 0; q < (LB == 2 ? RBq : NO); ++q) {
+            const int k1 = q + RBq * hb_;
+            const int x = k2b + N2 * k1;
+            if (k1 < NO && x < nx) {
+                ha_row[x] = u[q].x;
+                hb_row[x] = u[q].y;
             }
         }
     }
@@ -613,40 +629,43 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
         const T* tra = hm + ra * nx;
         const T* trb = hm + rb * nx;
         const bool va = ya < ny, vb = yb < ny;
-        constexpr int NZ = N2 / 2;
+        constexpr int NZ = RA / 2; // x < nx <= L/2: n2 < N2 / 2
 #pragma unroll
-        for (int n2 = 0; n2 < NZ; ++n2) {
-            const int x = n1 + N1 * n2;
+        for (int m = 0; m < NZ; ++m) {
+            const int x = n1 + N1 * (LA * m + ha);
             const bool in = x < nx;
-            v[n2] = cx<T>{(in && va) ? tra[x] : T(0), (in && vb) ? trb[x] : T(0)};
+            v[m] = cx<T>{(in && va) ? tra[x] : T(0), (in && vb) ? trb[x] : T(0)};
         }
-        DftP<N2, -1, NZ, N2>::run(v);
+        if constexpr (LA == 2) dft_pair<RA, -1, NZ>(v, ha);
+        else DftP<N2, -1, NZ, N2>::run(v);
     }
     __syncthreads(); // the exchange buffer overlays the tile
     if (a_task) {
         cx<T>* ex = sm + (pa * N2) * EX + n1;
 #pragma unroll
-        for (int k2 = 0; k2 < N2; ++k2) {
-            cx<T> w = v[k2];
+        for (int kk = 0; kk < RA; ++kk) {
+            const int k2 = kk + RA * ha;
+            cx<T> w = v[kk];
             if (k2 > 0) w = cmul(w, tws[k2 * N1 + n1]);
             ex[k2 * EX] = w;
         }
     }
     __syncthreads();
-    // ---- 3b. forward stage B -> natural-order Z rows (RB rounds, as in 1c)
+    // ---- 3b. forward stage B -> natural-order Z rows (RB rounds as in 1c)
 #pragma unroll 1
     for (int rnd = 0; rnd < X::RB; ++rnd) {
-        const int tb = tid + rnd * NT;
-        const int pb = tb / N2, k2 = tb % N2;
-        cx<T> u[N1];
-        const cx<T>* ex = sm + (pb * N2 + k2) * EX;
+        const int tb = tb0 + rnd * NT;
+        const int pb = tb / N2, k2b = tb % N2;
+        cx<T> u[RBq];
+        const cx<T>* ex = sm + (pb * N2 + k2b) * EX + hb_;
 #pragma unroll
-        for (int q = 0; q < N1; ++q) u[q] = ex[q];
-        DftP<N1, -1, N1, N1>::run(u);
+        for (int q = 0; q < RBq; ++q) u[q] = ex[LB * q];
+        if constexpr (LB == 2) dft_pair<RBq, -1, RBq>(u, hb_);
+        else DftP<N1, -1, N1, N1>::run(u);
         __syncthreads();
-        cx<T>* zr = sm + pb * ZP + k2;
+        cx<T>* zr = sm + pb * ZP + k2b;
 #pragma unroll
-        for (int k1 = 0; k1 < N1; ++k1) zr[N2 * k1] = u[k1];
+        for (int q = 0; q < RBq; ++q) zr[N2 * (q + RBq * hb_)] = u[q];
     }
     __syncthreads();
     // ---- 3c. separate the packed rows, write the next step's half spectra (kx-major)
