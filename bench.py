@@ -287,7 +287,8 @@ def run_b200_sharded(args, world, rank, local):
                 "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
                 "config": {"workload": wl, "nx": nx, "ny": ny, "nz": nz, "delta_nm": delta,
-                           "parallelism": f"z-slabs x{world} (NCCL all-to-all transposes + halo)",
+                           "parallelism": (f"z-slabs x{world} (NCCL all-to-all transposes + halo)" if world > 1
+                                           else "single GPU (one slab: no exchange)"),
                            "l2": "working set >> 126 MB L2; no flush", "cells": n},
                 "roofline": {"bound": "hbm", "kernel": "sharded_step", "achieved": achieved / world,
                              "peak": peak, "unit": "GB/s", "frac": achieved / world / peak, "traffic": None,

@@ -146,7 +146,8 @@ int mmb_device_bytes(mmb_ctx* ctx, size_t* out);
  * them in the same order); <m> is the global average. Field hooks (energy, max_torque,
  * effective_field, demag_field, tensor) are single-device only. mmb_create_emulated runs all
  * `world` ranks of the same decomposition on this process's device (exchanges by device
- * copies) and exposes the whole grid — used to test the sharded pipeline on one GPU. */
+ * copies) and exposes the whole grid — used to test the sharded pipeline on one GPU.
+ * With world == 1, mmb_create_sharded returns the single-device solver (nothing to exchange). */
 int mmb_nccl_unique_id(unsigned char out[128]);
 int mmb_create_sharded(const mmb_desc* desc, const mmb_stage* stages, int nstages, int rank,
                        int world, const unsigned char nccl_id[128], mmb_ctx** out);

@@ -802,7 +802,16 @@ int mmb_create_sharded(const mmb_desc* desc, const mmb_stage* stages, int nstage
     *out = nullptr;
     return guarded([&] {
         auto h = std::make_unique<mmb_ctx>();
-        h->s = mmb::make_sharded(*desc, stages, nstages, rank, world, nccl_id);
+        // one rank owns the whole grid: no exchange is needed, so the single-device solver
+        // runs it (MMB_FORCE_SHARDED=1 keeps the NCCL slab pipeline, for testing it)
+        const char* force = std::getenv("MMB_FORCE_SHARDED");
+        if (world == 1 && rank == 0 && !(force && force[0] == '1')) {
+            if (desc->precision == MMB_F64) h->s = std::make_unique<mmb::Solver<double>>(*desc, stages, nstages);
+            else if (desc->precision == MMB_F32) h->s = std::make_unique<mmb::Solver<float>>(*desc, stages, nstages);
+            else throw std::invalid_argument("unknown precision (expected MMB_F32 or MMB_F64)");
+        } else {
+            h->s = mmb::make_sharded(*desc, stages, nstages, rank, world, nccl_id);
+        }
         *out = h.release();
         return MMB_OK;
     });

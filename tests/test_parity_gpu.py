@@ -381,6 +381,7 @@ def test_nccl_sharded_single_rank_matches_single_device(monkeypatch):
     from paper_1501_07293_b200.simulation import make_sharded_simulation, nccl_unique_id
     sp = spec(24, 20, 12, 1.5, 1.3e7, 800.0, 30.0, 0.5, 5e-6, [(0, 100, (10.0, -20.0, 5.0))])
     monkeypatch.setenv("MMB_BIG_PATH", "1")
+    monkeypatch.setenv("MMB_FORCE_SHARDED", "1")  # world 1 otherwise runs the single-device solver
     single = b200(sp, "f32")
     rng = np.random.default_rng(11)
     v = rng.uniform(-1, 1, (3, 12, 20, 24))
