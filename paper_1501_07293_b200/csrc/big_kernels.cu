@@ -120,15 +120,14 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
 }
 
 // z pencils: W consecutive ky of one kx, all three components, Lz = 2^LOG2LZ >= 2 nz - 1.
-#ifndef MMB_ZW32
-#define MMB_ZW32 32
-#endif
-template <typename T>
-constexpr int zw() { return sizeof(T) == 4 ? MMB_ZW32 : 16; }
+// pencils per CTA: 32 (f32) keeps the tile at 98 KB (two CTAs per SM) up to Lz = 64; the
+// Lz = 128 tile halves it for the same occupancy
+template <typename T, int LOG2LZ>
+constexpr int zw() { return (sizeof(T) == 4 ? 32 : 16) >> (LOG2LZ >= 7 ? 1 : 0); }
 constexpr int kZThreads = 256;
 template <typename T, int LOG2LZ>
 constexpr int z_smem_bytes() {
-    return (2 * 3 * (1 << LOG2LZ) * zw<T>() + (1 << LOG2LZ)) * static_cast<int>(sizeof(cx<T>));
+    return (2 * 3 * (1 << LOG2LZ) * zw<T, LOG2LZ>() + (1 << LOG2LZ)) * static_cast<int>(sizeof(cx<T>));
 }
 
 template <typename T, int LOG2LZ>
@@ -139,7 +138,7 @@ __global__ void __launch_bounds__(kZThreads)
     // MAC, inverse DFT_N1, conj twiddle; then inverse stage A' (IDFT_N2 per (c, n1)) straight
     // to the nz live planes. Two shared buffers (A: [c][z][w], B: exchange), three barriers.
     using SP = Split<LOG2LZ>;
-    constexpr int LZ = SP::L, N1 = SP::N1, N2 = SP::N2, W = zw<T>();
+    constexpr int LZ = SP::L, N1 = SP::N1, N2 = SP::N2, W = zw<T, LOG2LZ>();
     constexpr int CS = LZ * W; // component stride in a tile buffer
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<T>* A = reinterpret_cast<cx<T>*>(smem_raw); // [c][z][w]
@@ -324,7 +323,7 @@ void launch_big_yi(const cx<T>* S2, cx<T>* S, const Geom& g, const cx<T>* tw, cu
 template <typename T>
 void launch_big_z(cx<T>* S2, const Geom& g, const cx<T>* tw, const T* kt, cudaStream_t stream) {
     switch (g.log2lz) {
-#define X(l) case l: { const dim3 grid((g.ly + zw<T>() - 1) / zw<T>(), g.xh); \
+#define X(l) case l: { const dim3 grid((g.ly + zw<T, l>() - 1) / zw<T, l>(), g.xh); \
         k_zmac<T, l><<<grid, kZThreads, z_smem_bytes<T, l>(), stream>>>(S2, g, tw, kt); break; }
         MMB_Z_CASES(X)
 #undef X
