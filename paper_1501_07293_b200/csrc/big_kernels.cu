@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
     const long long r0 = static_cast<long long>(blockIdx.x) * P;
     {
         // stage A: lane h of the task takes n2 = LA m + h
-        const int h = LA == 2 ? (tid & 1) : 0, task = LA == 2 ? (tid >> 1) : tid;
+        const int h = LA == 2 ? pair_half(tid) : 0, task = LA == 2 ? pair_task(tid) : tid;
         const int p = task / N1, n1 = task % N1;
         const long long r = r0 + p;
         cx<T> v[RA];
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
     // stage B: lane h of the task takes n1 = LB q + h; rows past nrows compute on zeros and
     // skip only their stores (the pair shuffles need every lane)
     for (int tb = tid; tb < P * N2 * LB; tb += NT) {
-        const int h = LB == 2 ? (tb & 1) : 0, task = LB == 2 ? (tb >> 1) : tb;
+        const int h = LB == 2 ? pair_half(tb) : 0, task = LB == 2 ? pair_task(tb) : tb;
         const int p = task / N2, k2 = task % N2;
         const long long r = r0 + p;
         cx<T> u[RB];

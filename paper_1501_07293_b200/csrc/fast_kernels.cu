@@ -435,6 +435,7 @@ struct XS {
     static constexpr int P = PAIR ? 3
                                   : (WIDE ? 3 * (PBE / SP::N1) : 3 * (SP::N2 >= PBE ? 1 : PBE / SP::N2));
     static constexpr int TR = 2 * P / 3;                                        // y rows per CTA
+    static constexpr bool ZFAST = TR >= 4;
     static constexpr int NT = WIDE ? P * SP::N1 : P * SP::N2 * LB;              // threads
     static_assert(P * SP::N1 * LA <= NT && P * SP::N2 * LB == NT * RB, "stage tasks");
     static constexpr int XHP = ((1 << LOG2L) / 2 + 1) | 1;            // staging pitch (odd)
@@ -446,6 +447,12 @@ struct XS {
 template <typename T, int LOG2L, int PB>
 constexpr int xs_smem_bytes() {
     return (XS<LOG2L, PB>::AREA + (1 << LOG2L)) * static_cast<int>(sizeof(cx<T>));
+}
+
+template <typename X>
+dim3 xs_grid(const Geom& g) {
+    const unsigned tiles = static_cast<unsigned>((g.ny + X::TR - 1) / X::TR);
+    return X::ZFAST ? dim3(g.nz, tiles) : dim3(tiles, g.nz);
 }
 
 template <typename T, int LOG2L, int PB>
@@ -470,7 +477,12 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
     T* hm = reinterpret_cast<T*>(smem_raw); // [3*TR][nx] tile: H_demag, then M_{t+1}
     cx<T>* tws = sm + X::AREA;
 
-    const int y0 = blockIdx.x * TR, z = blockIdx.y;
+    // ZFAST (tiles of >= 4 rows): z fastest in the grid, so the CTAs of one y tile in
+    // neighbouring planes run together and the +-z neighbour rows of the local terms come from
+    // L2 instead of DRAM re-reads. Narrower tiles keep y fastest: their 16-byte row segments
+    // of S share 32-byte sectors with the next tile, which must then run alongside.
+    const int z = X::ZFAST ? blockIdx.x : blockIdx.y;
+    const int y0 = (X::ZFAST ? blockIdx.y : blockIdx.x) * TR;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
     const long long cs = g.cs;
     const int zg = g.z0 + z, nzg = g.nz_g;
@@ -505,7 +517,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
     // h of a pair task takes n2 = LA m + h
     constexpr int LA = X::LA, LB = X::LB, RA = N2 / LA, RBq = N1 / LB;
     cx<T> v[RA];
-    const int ha = LA == 2 ? (tid & 1) : 0, ta = LA == 2 ? (tid >> 1) : tid;
+    const int ha = LA == 2 ? pair_half(tid) : 0, ta = LA == 2 ? pair_task(tid) : tid;
     const bool a_task = ta < P * N1;
     const int pa = ta / N1, n1 = ta % N1;
     if (a_task) {
@@ -543,7 +555,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
     __syncthreads();
     // ---- 1c. inverse stage B -> H_demag tile (the nx live cells); lane h of a pair task
     // takes n1 = LB q + h and returns k1 = q + RBq h
-    const int hb_ = LB == 2 ? (tid & 1) : 0, tb0 = LB == 2 ? (tid >> 1) : tid;
+    const int hb_ = LB == 2 ? pair_half(tid) : 0, tb0 = LB == 2 ? pair_task(tid) : tid;
     // RB = 2 (WIDE): the tile rows of round r lie inside exchange rows already consumed
     // (round 0: its own, synchronised below; round 1: round 0's), never in round 1's
 #pragma unroll 1
@@ -860,10 +872,10 @@ void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>
                        cudaStream_t stream, bool pdl) {
     const T coeff = static_cast<T>(exch_coeff), kan = static_cast<T>(aniso_coeff);
     switch (g.log2lx) {
-#define X(l) case l: if (xstep_small<l>(g)) { const dim3 grid((g.ny + XS<l, 16>::TR - 1) / XS<l, 16>::TR, g.nz); \
+#define X(l) case l: if (xstep_small<l>(g)) { const dim3 grid = xs_grid<XS<l, 16>>(g); \
         launch_pdl(pdl, k_xstep<T, l, 16>, grid, XS<l, 16>::NT, xs_smem_bytes<T, l, 16>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); \
         } else { if (xs_smem_bytes<T, l, MMB_XS_PB>() > 227 * 1024) throw std::invalid_argument("fast path: x tile exceeds shared memory"); \
-        const dim3 grid((g.ny + XS<l, MMB_XS_PB>::TR - 1) / XS<l, MMB_XS_PB>::TR, g.nz); \
+        const dim3 grid = xs_grid<XS<l, MMB_XS_PB>>(g); \
         launch_pdl(pdl, k_xstep<T, l, MMB_XS_PB>, grid, XS<l, MMB_XS_PB>::NT, xs_smem_bytes<T, l, MMB_XS_PB>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
         MMB_FAST_CASES(X)
 #undef X

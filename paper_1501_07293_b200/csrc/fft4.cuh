@@ -94,31 +94,37 @@ struct DftP {
     }
 };
 
-// Two-lane DFT of size 2R on the lane pair (l, l ^ 1), h = l & 1: on entry lane h holds the
-// DFT_R of x[2m + h] (its half, already transformed by DftP); on return it holds X[k + R h],
-// k < R. Radix-2 combine X[k] = E[k] + W_2R^k O[k], X[k + R] = E[k] - W_2R^k O[k]: the odd lane
-// twiddles, one shuffle swaps, each lane finishes its half with 2 FMA per value. Halves the
-// registers of a DFT_2R task (used for DFT_64 stages, R = 32). All 32 lanes must take part.
-template <int R, int SIGN, int K = 0>
+// Two-lane DFT of size 2R on the lane pair (l, l ^ XM), h = (l & XM) != 0: on entry lane h
+// holds the DFT_R of x[2m + h] (its half, already transformed by DftP); on return it holds
+// X[k + R h], k < R. Radix-2 combine X[k] = E[k] + W_2R^k O[k], X[k + R] = E[k] - W_2R^k O[k]:
+// the odd lane twiddles, one shuffle swaps, each lane finishes its half with 2 FMA per value.
+// Halves the registers of a DFT_2R task (used for DFT_64 stages, R = 32). With XM = 16 the two
+// halves sit in different half-warps, so each half-warp's shared-memory accesses stay
+// unit-stride across its 16 tasks. All 32 lanes must take part.
+template <int R, int SIGN, int XM, int K = 0>
 struct PairCombine {
     template <typename C, typename T>
     static __device__ __forceinline__ void run(C* v, int h, T sg) {
         if constexpr (K < R) {
             const C t = rot64<K * (32 / R), SIGN>(v[K]);
             const C mine = h ? t : v[K];
-            const T rx = __shfl_xor_sync(0xffffffffu, mine.x, 1);
-            const T ry = __shfl_xor_sync(0xffffffffu, mine.y, 1);
+            const T rx = __shfl_xor_sync(0xffffffffu, mine.x, XM);
+            const T ry = __shfl_xor_sync(0xffffffffu, mine.y, XM);
             v[K] = C{fmaf_t(sg, mine.x, rx), fmaf_t(sg, mine.y, ry)};
-            PairCombine<R, SIGN, K + 1>::run(v, h, sg);
+            PairCombine<R, SIGN, XM, K + 1>::run(v, h, sg);
         }
     }
 };
-template <int R, int SIGN, int NZH, typename C>
+template <int R, int SIGN, int NZH, int XM = 16, typename C>
 __device__ __forceinline__ void dft_pair(C* v, int h) {
     using T = decltype(v[0].x);
     DftP<R, SIGN, NZH, R>::run(v);
-    PairCombine<R, SIGN>::run(v, h, h ? T(-1) : T(1));
+    PairCombine<R, SIGN, XM>::run(v, h, h ? T(-1) : T(1));
 }
+// Lane-pair task mapping for dft_pair<..., 16>: half h = bit 4 of the lane, task index =
+// 16 per warp.
+__device__ __forceinline__ int pair_half(int t) { return (t >> 4) & 1; }
+__device__ __forceinline__ int pair_task(int t) { return ((t >> 5) << 4) | (t & 15); }
 
 // Smem index padding for a row of length L = N1*N2 processed by the four-step: one slot
 // per N1 elements, so stage-B reads at stride N1 become stride N1+1 (conflict free).
