@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
     cx<T>* tws = sm + P * N2 * EX;
     if (prologue && blockIdx.x == 0 && threadIdx.x == 0) step_prologue(ctl, st, prologue);
     stage_twiddles<T, LOG2L>(tws, tw);
+    cp_async_wait_all();
     __syncthreads();
     const int tid = threadIdx.x;
     const long long r0 = static_cast<long long>(blockIdx.x) * P;

@@ -77,10 +77,15 @@ __device__ __forceinline__ void load6(const T* __restrict__ p, T (&k)[6]) {
 // n1-consecutive lanes of stage A: bank-conflict free, no global loads on the hot path).
 template <typename T, int LOG2L>
 __device__ __forceinline__ void stage_twiddles(cx<T>* tws, const cx<T>* __restrict__ tw) {
-    using SP = Split<LOG2L>;
-    for (int e = threadIdx.x; e < SP::L; e += blockDim.x) {
-        const int k2 = e / SP::N1, n1 = e % SP::N1;
-        tws[e] = __ldg(&tw[n1 * k2]);
+    // async copies of the table's [k2][n1] copy (tw[L..2L), launch_twiddles): the caller's
+    // cp_async_wait_all + barrier completes them
+    constexpr int L = 1 << LOG2L;
+    constexpr int PER = 16 / static_cast<int>(sizeof(cx<T>));
+    const cx<T>* src = tw + L;
+    if (L % PER == 0 && (static_cast<unsigned>(__cvta_generic_to_shared(tws)) & 15u) == 0) {
+        for (int e = threadIdx.x * PER; e < L; e += blockDim.x * PER) cp_async<16>(tws + e, src + e);
+    } else {
+        for (int e = threadIdx.x; e < L; e += blockDim.x) cp_async<sizeof(cx<T>)>(tws + e, src + e);
     }
 }
 

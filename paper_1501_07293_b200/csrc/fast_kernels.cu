@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
     if (prologue && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
         step_prologue(ctl, st, prologue);
     stage_twiddles<T, LOG2L>(tws, tw);
+    cp_async_wait_all();
     __syncthreads();
 
     const int y0 = blockIdx.x * (2 * P), z = blockIdx.y, c = blockIdx.z;
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
     if (!bulk) {
         for (int e = tid; e < rows * ny; e += NT) sm[(e / ny) * RP + e % ny] = gblk[e];
     }
+    cp_async_wait_all();
     __syncthreads();
     if (bulk) mbar_wait(&bar, 0);
 

@@ -72,6 +72,7 @@ void launch_cs_table(double2* cs, int L, cudaStream_t stream);
 template <typename T>
 void launch_tensor_finalize(const double* spec, T* out, long long count, double scale,
                             cudaStream_t stream);
+// tw[2L]: W_L^t (t < L), then the same values in four-step [k2][n1] order (tw + L).
 template <typename T>
 void launch_twiddles(cx<T>* tw, int L, cudaStream_t stream);
 

@@ -442,9 +442,9 @@ private:
         if (R->ncols > 0)
             ck(cudaMemcpyAsync(R->kspec.p, kfull.p + R->k0 * per_kx, R->ncols * per_kx * sizeof(T),
                                cudaMemcpyDeviceToDevice, stream_), "tensor slice");
-        R->twx.alloc(g_.lx);
-        R->twy.alloc(g_.ly);
-        R->twz.alloc(g_.lz);
+        R->twx.alloc(2 * g_.lx);
+        R->twy.alloc(2 * g_.ly);
+        R->twz.alloc(2 * g_.lz);
         launch_twiddles<T>(R->twx.p, g_.lx, stream_);
         launch_twiddles<T>(R->twy.p, g_.ly, stream_);
         launch_twiddles<T>(R->twz.p, g_.lz, stream_);

@@ -100,9 +100,9 @@ public:
                       : static_cast<size_t>(3) * g.nz * g.ly * g.xp);
         if (fast_ && !yz_) S2_.alloc(static_cast<size_t>(3) * g.nz * g.ly * g.xh);
         kspec_.alloc(static_cast<size_t>(6) * g.zh * g.yh * g.xh);
-        twx_.alloc(g.lx);
-        twy_.alloc(g.ly);
-        twz_.alloc(g.lz);
+        twx_.alloc(2 * g.lx);
+        twy_.alloc(2 * g.ly);
+        twz_.alloc(2 * g.lz);
         partial_.alloc(3 * 1024);
         tpart_count_ = fast_ ? fast_xstep_blocks<T>(g) : llg_blocks(g);
         tpart_.alloc(std::max(llg_blocks(g), tpart_count_));

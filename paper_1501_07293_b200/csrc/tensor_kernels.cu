@@ -103,13 +103,20 @@ __global__ void k_finalize_fast(const double* __restrict__ spec, T* __restrict__
         static_cast<T>(sgn * scale * spec[c * count + f]);
 }
 
-// W_L^t = exp(-2 pi i t / L), fp64 sincospi then narrowed.
+// tw[t] = W_L^t = exp(-2 pi i t / L) for t < L, fp64 sincospi then narrowed; then
+// tw[L + k2 * N1 + n1] = W_L^(n1 k2), the same values in the [k2][n1] order of the register
+// four-step (fft4.cuh Split), which the kernels copy to shared memory with async bulk copies.
 template <typename T>
-__global__ void k_twiddles(cx<T>* tw, int L) {
+__global__ void k_twiddles(cx<T>* tw, int L, int log2n1) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= L) return;
+    if (t >= 2 * L) return;
+    int e = t;
+    if (t >= L) {
+        const int f = t - L, n1 = f & ((1 << log2n1) - 1), k2 = f >> log2n1;
+        e = n1 * k2;
+    }
     double s, c;
-    sincospi(2.0 * static_cast<double>(t) / static_cast<double>(L), &s, &c);
+    sincospi(2.0 * static_cast<double>(e) / static_cast<double>(L), &s, &c);
     tw[t] = cx<T>{static_cast<T>(c), static_cast<T>(-s)};
 }
 
@@ -151,7 +158,9 @@ void launch_tensor_finalize_fast(const double* spec, T* out, int xh, int yh, int
 
 template <typename T>
 void launch_twiddles(cx<T>* tw, int L, cudaStream_t stream) {
-    k_twiddles<T><<<(L + 255) / 256, 256, 0, stream>>>(tw, L);
+    int log2l = 0;
+    while ((1 << log2l) < L) ++log2l;
+    k_twiddles<T><<<(2 * L + 255) / 256, 256, 0, stream>>>(tw, L, log2l / 2);
     check_launch();
 }
 
