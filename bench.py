@@ -136,8 +136,16 @@ def dist_setup():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        ndev = max(1, torch.cuda.device_count())
+        if world <= ndev:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
+        else:
+            # more ranks than GPUs (only to exercise the multi-rank code path on a small box):
+            # ranks share devices, collectives over gloo; timings are then contended
+            local = local % ndev
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -152,7 +160,8 @@ def max_over_ranks(world, v):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -162,7 +171,7 @@ def sum_over_ranks(world, v):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -246,7 +255,8 @@ def run_b200_sharded(args, world, rank, local):
     nx, ny, nz, delta, a_ex, ms, hk, alpha, dt, prec = WORKLOADS[wl]
     w = 4 if prec == "f32" else 8
     n = nx * ny * nz
-    nid = torch.zeros(128, dtype=torch.uint8, device="cuda" if world > 1 else "cpu")
+    nid = torch.zeros(128, dtype=torch.uint8,
+                      device="cuda" if world > 1 and dist.get_backend() == "nccl" else "cpu")
     if rank == 0:
         nid[:] = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8)
     if world > 1:
