@@ -160,6 +160,7 @@ public:
         for (auto& ge : batch_)
             if (ge) cudaGraphExecDestroy(ge);
         if (ctl_host_) cudaFreeHost(ctl_host_);
+        if (rec_host_) cudaFreeHost(rec_host_);
         if (stream_) cudaStreamDestroy(stream_);
     }
 
@@ -252,6 +253,7 @@ public:
         const double ms2 = d_.ms * d_.ms;
         long long done = 0;
         const bool stop = stop_torque >= 0.0;
+        if (fn && cadence > 0 && !stop) return run_streaming(steps, cadence, fn, user);
         while (done < steps) {
             // Batch graph replays up to the next record point when no per-step check is needed.
             long long chunk = steps - done;
@@ -271,6 +273,48 @@ public:
     }
 
     void synchronize() override { sync_and_check(); }
+
+    // run() without a torque stop: each record's <m> sums go into a device ring right behind
+    // the graph replays (no host round trip per record); the ring is copied back and delivered
+    // to `fn` in order every kRing records and at the end. If a step failed, the records taken
+    // before the failing step are delivered first, then the error is raised as usual.
+    long long run_streaming(long long steps, long long cadence, mmb_record_fn fn, void* user) {
+        constexpr int kRing = 256;
+        if (!rec_.p) {
+            rec_.alloc(3 * kRing);
+            ck(cudaMallocHost(&rec_host_, 3 * kRing * sizeof(double)), "cudaMallocHost");
+        }
+        long long rsteps[kRing];
+        int nrec = 0;
+        const double inv = 1.0 / static_cast<double>(g_.n), inv_ms = 1.0 / d_.ms;
+        auto flush = [&]() {
+            if (nrec) ck(cudaMemcpyAsync(rec_host_, rec_.p, 3 * nrec * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+                         "records");
+            ck(cudaStreamSynchronize(stream_), "sync");
+            fetch_ctl();
+            const unsigned long long key = ctl_host_->bad_key;
+            const long long fail = key != ~0ull ? static_cast<long long>(key >> 36) : (1LL << 62);
+            for (int i = 0; i < nrec && rsteps[i] <= fail; ++i) {
+                const double* s = rec_host_ + 3 * i;
+                fn(user, rsteps[i], (inv * s[0]) * inv_ms, (inv * s[1]) * inv_ms, (inv * s[2]) * inv_ms);
+            }
+            nrec = 0;
+            check_numerical();
+        };
+        long long done = 0;
+        while (done < steps) {
+            const long long chunk = std::min(steps - done, cadence - (step_ % cadence));
+            step(chunk);
+            done += chunk;
+            if (step_ % cadence == 0) {
+                launch_sum3<T>(m_[cur_].p, g_.n, g_.n, partial_.p, rec_.p + 3 * nrec, stream_);
+                rsteps[nrec++] = step_;
+                if (nrec == kRing) flush();
+            }
+        }
+        flush();
+        return done;
+    }
 
     void effective_field(void* x, void* y, void* z) override {
         enqueue_heff();
@@ -571,7 +615,8 @@ private:
     DevBuf<T> m_[2], hd_, heff_;
     DevBuf<cx<T>> S_, S2_, twx_, twy_, twz_;
     DevBuf<T> kspec_;
-    DevBuf<double> partial_, red_, tpart_;
+    DevBuf<double> partial_, red_, tpart_, rec_;
+    double* rec_host_ = nullptr;
     DevBuf<StepCtl> ctl_;
     StepCtl* ctl_host_ = nullptr;
     cudaGraphExec_t graph_[2] = {nullptr, nullptr};

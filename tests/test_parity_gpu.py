@@ -210,6 +210,32 @@ def test_degenerate_cell_is_numerical_error():
         sim.average_unit()
 
 
+def test_streamed_records_match_per_step_averages():
+    """run() without a torque stop streams <m> sums through a device ring (flushed every 256
+    records): 600 records at cadence 1 equal step(1) + average_unit() bitwise."""
+    recs = []
+    s1 = b200(tiny_relaxation())
+    assert s1.run(RunOptions(steps=600, cadence=1, sink=recs.append)) == 600
+    s2 = b200(tiny_relaxation())
+    want = []
+    for k in range(1, 601):
+        s2.step(1)
+        want.append((k,) + tuple(s2.average_unit()))
+    assert [(r.step, r.mx, r.my, r.mz) for r in recs] == want
+
+
+def test_streamed_records_stop_at_the_failing_step():
+    sp = spec(2, 1, 1, 1.0, 0.0, 800.0, 0.0, 0.5, 1e-5)
+    sim = b200(sp)
+    m = sim.magnetization()
+    m[:, 0, 0, 1] = 0.0
+    sim.set_magnetization(m)
+    recs = []
+    with pytest.raises(NumericalError, match=r"at cell 1 at step 0"):
+        sim.run(RunOptions(steps=10, cadence=1, sink=recs.append))
+    assert recs == []  # the first step failed: no record was taken before it
+
+
 def test_argument_errors():
     with pytest.raises(ValueError):
         b200(spec(4, 4, 1, 1.0, ms=-1.0))
