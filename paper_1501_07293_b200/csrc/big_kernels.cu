@@ -152,12 +152,29 @@ __global__ void __launch_bounds__(kZThreads)
     const long long zpitch = ly;
     cx<T>* blk = S2 + static_cast<long long>(kx) * 3 * nz * ly + ky0;
 
-    // load the nz live planes (async, coalesced over ky)
-    for (int e = tid; e < 3 * nz * W; e += kZThreads) {
-        const int w = e % W, cz = e / W, c = cz / nz, z = cz - c * nz;
-        cx<T>* d = A + (c * LZ + z) * W + w;
-        if (w < wl) cp_async<sizeof(cx<T>)>(d, blk + (c * nz + z) * zpitch + w);
-        else *d = cx<T>{0, 0};
+    // load the nz live planes (async, coalesced over ky): each thread keeps its w and walks
+    // the (c, z) planes with a fixed stride, carrying (c, z) instead of dividing
+    {
+        static_assert(kZThreads % W == 0, "pencil tile");
+        constexpr int CZSTEP = kZThreads / W;
+        const int w = tid % W;
+        int c = 0, z = tid / W;
+        while (z >= nz) {
+            z -= nz;
+            ++c;
+        }
+        const cx<T>* src = blk + static_cast<long long>(tid / W) * zpitch + w;
+        for (int cz = tid / W; cz < 3 * nz; cz += CZSTEP) {
+            cx<T>* d = A + (c * LZ + z) * W + w;
+            if (w < wl) cp_async<sizeof(cx<T>)>(d, src);
+            else *d = cx<T>{0, 0};
+            src += CZSTEP * zpitch;
+            z += CZSTEP;
+            while (z >= nz) {
+                z -= nz;
+                ++c;
+            }
+        }
     }
     stage_twiddles<T, LOG2LZ>(tws, tw);
     cp_async_wait_all();
