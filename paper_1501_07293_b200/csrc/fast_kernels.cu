@@ -438,8 +438,16 @@ struct XS {
                                   : (WIDE ? 3 * (PBE / SP::N1) : 3 * (SP::N2 >= PBE ? 1 : PBE / SP::N2));
     static constexpr int TR = 2 * P / 3;                                        // y rows per CTA
     static constexpr bool ZFAST = TR >= 4;
-    static constexpr int NT = WIDE ? P * SP::N1 : P * SP::N2 * LB;              // threads
-    static_assert(P * SP::N1 * LA <= NT && P * SP::N2 * LB == NT * RB, "stage tasks");
+    static constexpr int NT0 = WIDE ? P * SP::N1 : P * SP::N2 * LB; // threads with FFT tasks
+    // small-grid tiles (PB <= 16) get TM times the threads: the extra ones only take part in
+    // the staging, local-term and spectrum-store loops, which otherwise run 5+ cells deep
+#ifndef MMB_XS_TM_THREADS
+#define MMB_XS_TM_THREADS 192
+#endif
+    static constexpr int TM = (PB <= 16 && LA == 1 && LB == 1 && NT0 < MMB_XS_TM_THREADS) ? MMB_XS_TM_THREADS / NT0 : 1;
+    static constexpr int NT = NT0 * TM;                                         // threads
+    static_assert(P * SP::N1 * LA <= NT0 && P * SP::N2 * LB == NT0 * RB, "stage tasks");
+    static_assert(TM == 1 || (LA == 1 && LB == 1), "pair shuffles need every lane");
     static constexpr int XHP = ((1 << LOG2L) / 2 + 1) | 1;            // staging pitch (odd)
     static constexpr int EX = SP::N1 + 1;
     static constexpr int ZP = (1 << LOG2L) + 1;
@@ -563,24 +571,29 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
 #pragma unroll 1
     for (int rnd = 0; rnd < X::RB; ++rnd) {
         const int tb = tb0 + rnd * NT;
+        const bool b_task = X::TM == 1 || tb < P * N2 * LB;
         const int pb = tb / N2, k2b = tb % N2;
         cx<T> u[RBq];
-        const cx<T>* ex = sm + (pb * N2 + k2b) * EX + hb_;
-#pragma unroll
-        for (int q = 0; q < RBq; ++q) u[q] = ex[LB * q];
         constexpr int NO = N1 == 1 ? 1 : N1 / 2;
-        if constexpr (LB == 2) dft_pair<RBq, +1, RBq>(u, hb_);
-        else DftP<N1, +1, N1, NO>::run(u);
-        __syncthreads(); // the tile overlays the exchange buffer
-        T* ha_row = hm + (2 * pb) * nx;
-        T* hb_row = ha_row + nx;
+        if (b_task) {
+            const cx<T>* ex = sm + (pb * N2 + k2b) * EX + hb_;
 #pragma unroll
-        for (int q = 0; q < (LB == 2 ? RBq : NO); ++q) {
-            const int k1 = q + RBq * hb_;
-            const int x = k2b + N2 * k1;
-            if (k1 < NO && x < nx) {
-                ha_row[x] = u[q].x;
-                hb_row[x] = u[q].y;
+            for (int q = 0; q < RBq; ++q) u[q] = ex[LB * q];
+            if constexpr (LB == 2) dft_pair<RBq, +1, RBq>(u, hb_);
+            else DftP<N1, +1, N1, NO>::run(u);
+        }
+        __syncthreads(); // the tile overlays the exchange buffer
+        if (b_task) {
+            T* ha_row = hm + (2 * pb) * nx;
+            T* hb_row = ha_row + nx;
+#pragma unroll
+            for (int q = 0; q < (LB == 2 ? RBq : NO); ++q) {
+                const int k1 = q + RBq * hb_;
+                const int x = k2b + N2 * k1;
+                if (k1 < NO && x < nx) {
+                    ha_row[x] = u[q].x;
+                    hb_row[x] = u[q].y;
+                }
             }
         }
     }
@@ -669,17 +682,22 @@ __global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>
 #pragma unroll 1
     for (int rnd = 0; rnd < X::RB; ++rnd) {
         const int tb = tb0 + rnd * NT;
+        const bool b_task = X::TM == 1 || tb < P * N2 * LB;
         const int pb = tb / N2, k2b = tb % N2;
         cx<T> u[RBq];
-        const cx<T>* ex = sm + (pb * N2 + k2b) * EX + hb_;
+        if (b_task) {
+            const cx<T>* ex = sm + (pb * N2 + k2b) * EX + hb_;
 #pragma unroll
-        for (int q = 0; q < RBq; ++q) u[q] = ex[LB * q];
-        if constexpr (LB == 2) dft_pair<RBq, -1, RBq>(u, hb_);
-        else DftP<N1, -1, N1, N1>::run(u);
+            for (int q = 0; q < RBq; ++q) u[q] = ex[LB * q];
+            if constexpr (LB == 2) dft_pair<RBq, -1, RBq>(u, hb_);
+            else DftP<N1, -1, N1, N1>::run(u);
+        }
         __syncthreads();
-        cx<T>* zr = sm + pb * ZP + k2b;
+        if (b_task) {
+            cx<T>* zr = sm + pb * ZP + k2b;
 #pragma unroll
-        for (int q = 0; q < RBq; ++q) zr[N2 * (q + RBq * hb_)] = u[q];
+            for (int q = 0; q < RBq; ++q) zr[N2 * (q + RBq * hb_)] = u[q];
+        }
     }
     __syncthreads();
     // ---- 3c. separate the packed rows, write the next step's half spectra (kx-major)
