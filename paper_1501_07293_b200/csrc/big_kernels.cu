@@ -44,11 +44,11 @@ constexpr int yr_smem_bytes() {
 
 // Row FFT along y. INV = 0: in rows hold n_live values (pitch in_pitch), out rows get all L
 // values. INV = 1: in rows hold L values, out rows get the first n_live values.
-template <typename T, int LOG2L, int INV>
+template <typename T, int LOG2L, int INV, bool PEER = false>
 __global__ void __launch_bounds__(YR<LOG2L>::NT)
     k_yrow(const cx<T>* __restrict__ in, cx<T>* __restrict__ out, long long nrows, int in_pitch,
            int out_pitch, int n_live, const cx<T>* __restrict__ tw, StepCtl* ctl, StageTable st,
-           int prologue) {
+           int prologue, RowMap<T> rm, int nzr) {
     using SP = Split<LOG2L>;
     using Y = YR<LOG2L>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = Y::P, EX = Y::EX, NT = Y::NT;
@@ -73,7 +73,10 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
 #pragma unroll
         for (int m = 0; m < RA; ++m) v[m] = cx<T>{0, 0};
         if (r < nrows) {
-            const cx<T>* src = in + r * in_pitch;
+            // forward rows may live in the ranks' slab spectra (RowMap; row = (kx, c, z))
+            const cx<T>* src = (!INV && PEER) ? rm.row(static_cast<int>(r / (3 * nzr)), static_cast<int>(r / nzr % 3),
+                                                           static_cast<int>(r % nzr), in_pitch)
+                                                  : in + r * in_pitch;
 #pragma unroll
             for (int m = 0; m < NZ; ++m) {
                 const int y = n1 + N1 * (LA * m + h);
@@ -105,7 +108,9 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
         if constexpr (LB == 2) dft_pair<RB, SIGN, RB>(u, h);
         else DftP<N1, SIGN, N1, (INV && N1 > 1) ? N1 / 2 : N1>::run(u);
         if (r < nrows) {
-            cx<T>* dst = out + r * out_pitch;
+            cx<T>* dst = (INV && PEER) ? rm.row(static_cast<int>(r / (3 * nzr)), static_cast<int>(r / nzr % 3),
+                                                    static_cast<int>(r % nzr), out_pitch)
+                                           : out + r * out_pitch;
 #pragma unroll
             for (int q = 0; q < RB; ++q) {
                 const int k1 = q + RB * h;
@@ -295,7 +300,8 @@ bool big_supported(const Geom& g) {
 template <typename T>
 void prepare_big_kernels(const Geom& g) {
     switch (g.log2ly) {
-#define X(l) case l: set_smem(k_yrow<T, l, 0>, yr_smem_bytes<T, l>()); set_smem(k_yrow<T, l, 1>, yr_smem_bytes<T, l>()); break;
+#define X(l) case l: set_smem(k_yrow<T, l, 0>, yr_smem_bytes<T, l>()); set_smem(k_yrow<T, l, 1>, yr_smem_bytes<T, l>()); \
+                     set_smem(k_yrow<T, l, 0, true>, yr_smem_bytes<T, l>()); set_smem(k_yrow<T, l, 1, true>, yr_smem_bytes<T, l>()); break;
         MMB_Y_CASES(X)
 #undef X
         default: throw std::invalid_argument("big path: bad Ly");
@@ -310,12 +316,17 @@ void prepare_big_kernels(const Geom& g) {
 
 template <typename T>
 void launch_big_yf(const cx<T>* S, cx<T>* S2, const Geom& g, const cx<T>* tw, StepCtl* ctl,
-                   const StageTable& st, int prologue, cudaStream_t stream) {
+                   const StageTable& st, int prologue, cudaStream_t stream, const RowMap<T>* rows) {
     const long long nrows = static_cast<long long>(g.xh) * 3 * g.nz;
+    RowMap<T> rm{};
+    if (rows) rm = *rows;
     switch (g.log2ly) {
 #define X(l) case l: { constexpr int P = YR<l>::P; \
-        k_yrow<T, l, 0><<<static_cast<unsigned>((nrows + P - 1) / P), YR<l>::NT, yr_smem_bytes<T, l>(), stream>>>( \
-            S, S2, nrows, g.ny, g.ly, g.ny, tw, ctl, st, prologue); break; }
+        const unsigned grid = static_cast<unsigned>((nrows + P - 1) / P); \
+        if (rows) k_yrow<T, l, 0, true><<<grid, YR<l>::NT, yr_smem_bytes<T, l>(), stream>>>( \
+            S, S2, nrows, g.ny, g.ly, g.ny, tw, ctl, st, prologue, rm, g.nz); \
+        else k_yrow<T, l, 0><<<grid, YR<l>::NT, yr_smem_bytes<T, l>(), stream>>>( \
+            S, S2, nrows, g.ny, g.ly, g.ny, tw, ctl, st, prologue, rm, g.nz); break; }
         MMB_Y_CASES(X)
 #undef X
         default: throw std::invalid_argument("big path: bad Ly");
@@ -324,13 +335,19 @@ void launch_big_yf(const cx<T>* S, cx<T>* S2, const Geom& g, const cx<T>* tw, St
 }
 
 template <typename T>
-void launch_big_yi(const cx<T>* S2, cx<T>* S, const Geom& g, const cx<T>* tw, cudaStream_t stream) {
+void launch_big_yi(const cx<T>* S2, cx<T>* S, const Geom& g, const cx<T>* tw, cudaStream_t stream,
+                   const RowMap<T>* rows) {
     const long long nrows = static_cast<long long>(g.xh) * 3 * g.nz;
+    RowMap<T> rm{};
+    if (rows) rm = *rows;
     StageTable st{};
     switch (g.log2ly) {
 #define X(l) case l: { constexpr int P = YR<l>::P; \
-        k_yrow<T, l, 1><<<static_cast<unsigned>((nrows + P - 1) / P), YR<l>::NT, yr_smem_bytes<T, l>(), stream>>>( \
-            S2, S, nrows, g.ly, g.ny, g.ny, tw, nullptr, st, 0); break; }
+        const unsigned grid = static_cast<unsigned>((nrows + P - 1) / P); \
+        if (rows) k_yrow<T, l, 1, true><<<grid, YR<l>::NT, yr_smem_bytes<T, l>(), stream>>>( \
+            S2, S, nrows, g.ly, g.ny, g.ny, tw, nullptr, st, 0, rm, g.nz); \
+        else k_yrow<T, l, 1><<<grid, YR<l>::NT, yr_smem_bytes<T, l>(), stream>>>( \
+            S2, S, nrows, g.ly, g.ny, g.ny, tw, nullptr, st, 0, rm, g.nz); break; }
         MMB_Y_CASES(X)
 #undef X
         default: throw std::invalid_argument("big path: bad Ly");
@@ -354,8 +371,9 @@ void launch_big_z(cx<T>* S2, const Geom& g, const cx<T>* tw, const T* kt, cudaSt
     template bool big_supported<T>(const Geom&);                                                 \
     template void prepare_big_kernels<T>(const Geom&);                                           \
     template void launch_big_yf<T>(const cx<T>*, cx<T>*, const Geom&, const cx<T>*, StepCtl*,     \
-                                   const StageTable&, int, cudaStream_t);                        \
-    template void launch_big_yi<T>(const cx<T>*, cx<T>*, const Geom&, const cx<T>*, cudaStream_t); \
+                                   const StageTable&, int, cudaStream_t, const RowMap<T>*);      \
+    template void launch_big_yi<T>(const cx<T>*, cx<T>*, const Geom&, const cx<T>*, cudaStream_t, \
+                                   const RowMap<T>*);                                            \
     template void launch_big_z<T>(cx<T>*, const Geom&, const cx<T>*, const T*, cudaStream_t);
 #ifndef MMB_ONLY_F64
 MMB_BINST(float)

@@ -10,6 +10,26 @@
 
 namespace mmb {
 
+// Rows of the y/z stage read from and written back to the ranks' own slab spectra instead of a
+// transposed column buffer (peer-memory sharding, shard.cu): row (kx, c, z) of this rank's
+// column range lives in rank q = owner(z) at base[q][((k0 + kx) * 3 + c) * nzl_q + z - z0[q]]
+// rows of ny values. base[q] may be another GPU's memory (CUDA IPC, NVLink loads/stores).
+// world == 0: rows are the contiguous local column buffer.
+constexpr int kMaxRanks = 8;
+template <typename T>
+struct RowMap {
+    cx<T>* base[kMaxRanks];
+    int z0[kMaxRanks + 1]; // slab starts, z0[world] = nz
+    int world = 0;
+    int k0 = 0;
+    __device__ __forceinline__ cx<T>* row(int kx, int c, int z, int ny) const {
+        int q = 0;
+        while (z >= z0[q + 1]) ++q;
+        const long long nzl = z0[q + 1] - z0[q];
+        return base[q] + ((static_cast<long long>(k0 + kx) * 3 + c) * nzl + (z - z0[q])) * ny;
+    }
+};
+
 template <typename T> bool fast_supported(const Geom& g);
 template <typename T> int fast_yz_kxb(const Geom& g, int* smem_bytes);
 template <typename T> void prepare_fast_kernels(const Geom& g);
@@ -19,7 +39,8 @@ void launch_fast_xf(const T* m, cx<T>* S, const Geom& g, const cx<T>* tw, StepCt
 // KYZ; block 0 optionally runs the step prologue (schedule, sticky alpha, prefactors).
 template <typename T>
 void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, StepCtl* ctl,
-                    const StageTable& st, int prologue, cudaStream_t stream, bool pdl = false);
+                    const StageTable& st, int prologue, cudaStream_t stream, bool pdl = false,
+                    const RowMap<T>* rows = nullptr);
 // KXS: fused x-c2r -> local terms + LLG update (M -> mout) -> x-r2c of mout, S in place.
 // Writes one torque partial per CTA (fast_xstep_blocks of them) to tpart.
 template <typename T>
@@ -41,10 +62,11 @@ template <typename T> bool big_supported(const Geom& g);
 template <typename T> void prepare_big_kernels(const Geom& g);
 template <typename T>
 void launch_big_yf(const cx<T>* S, cx<T>* S2, const Geom& g, const cx<T>* tw, StepCtl* ctl,
-                   const StageTable& st, int prologue, cudaStream_t stream);
+                   const StageTable& st, int prologue, cudaStream_t stream, const RowMap<T>* rows = nullptr);
 template <typename T>
 void launch_big_z(cx<T>* S2, const Geom& g, const cx<T>* tw, const T* kt, cudaStream_t stream);
 template <typename T>
-void launch_big_yi(const cx<T>* S2, cx<T>* S, const Geom& g, const cx<T>* tw, cudaStream_t stream);
+void launch_big_yi(const cx<T>* S2, cx<T>* S, const Geom& g, const cx<T>* tw, cudaStream_t stream,
+                   const RowMap<T>* rows = nullptr);
 
 } // namespace mmb

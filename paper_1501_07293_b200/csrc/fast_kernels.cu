@@ -223,10 +223,10 @@ constexpr int yz_threads() {
     return n2 >= 384 ? n2 : (384 / n2) * n2;
 }
 
-template <typename T, int LOG2L, int ZM>
+template <typename T, int LOG2L, int ZM, bool PEER = false>
 __global__ void __launch_bounds__(yz_threads<LOG2L>())
     k_yz(cx<T>* __restrict__ S, Geom g, const cx<T>* __restrict__ tw, const T* __restrict__ kt,
-         int kxb, StepCtl* ctl, StageTable st, int prologue) {
+         int kxb, StepCtl* ctl, StageTable st, int prologue, RowMap<T> rm) {
     using SP = Split<LOG2L>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2;
     constexpr int RP = fpitch<LOG2L>();
@@ -246,10 +246,20 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
     const int rows = kxn * 3 * nz;
     const int tid = threadIdx.x;
     cx<T>* gblk = S + sf_row(kx0, 0, 0, nz, ny); // rows of this CTA are contiguous in S
+    // row r of the block: in S, or in the owning rank's slab spectrum (RowMap, peer memory)
+    auto grow = [&](int r) -> cx<T>* {
+        if constexpr (!PEER) {
+            return gblk + static_cast<long long>(r) * ny;
+        } else {
+            const int kxl = r / (3 * nz), rc = r - kxl * 3 * nz;
+            return rm.row(kx0 + kxl, rc / nz, rc % nz, ny);
+        }
+    };
     // TMA bulk copies of all live input rows (ny values each) into the first ny slots of
-    // their shared-memory rows, in flight together while the twiddles are staged.
+    // their shared-memory rows, in flight together while the twiddles are staged. Rows in
+    // peer memory are read with plain loads.
     const unsigned rowbytes = static_cast<unsigned>(ny * sizeof(cx<T>));
-    const bool bulk = (rowbytes % 16) == 0;
+    const bool bulk = (rowbytes % 16) == 0 && !PEER;
     if (tid == 0) {
         mbar_init(&bar, 1);
         if (bulk) {
@@ -259,7 +269,7 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
     }
     stage_twiddles<T, LOG2L>(tws, tw);
     if (!bulk) {
-        for (int e = tid; e < rows * ny; e += NT) sm[(e / ny) * RP + e % ny] = gblk[e];
+        for (int e = tid; e < rows * ny; e += NT) sm[(e / ny) * RP + e % ny] = grow(e / ny)[e % ny];
     }
     cp_async_wait_all();
     __syncthreads();
@@ -402,7 +412,7 @@ __global__ void __launch_bounds__(yz_threads<LOG2L>())
             for (int q = 0; q < N1; ++q) u[q] = src[fpad<LOG2L>(k2 * N1 + q)];
             constexpr int NO = N1 == 1 ? 1 : N1 / 2;
             DftP<N1, +1, N1, NO>::run(u);
-            cx<T>* dst = gblk + static_cast<long long>(rbr) * ny;
+            cx<T>* dst = grow(rbr);
 #pragma unroll
             for (int k1 = 0; k1 < NO; ++k1) {
                 const int y = k2 + N2 * k1;
@@ -818,7 +828,8 @@ void prepare_fast_kernels(const Geom& g) {
     int sb = 0;
     fast_yz_kxb<T>(g, &sb);
     switch (g.log2ly) {
-#define X(l) case l: set_smem(k_yz<T, l, 0>, sb); if constexpr (sizeof(T) == 4) set_smem(k_yz<T, l, 1>, sb); break;
+#define X(l) case l: set_smem(k_yz<T, l, 0>, sb); set_smem(k_yz<T, l, 0, true>, sb); \
+                     if constexpr (sizeof(T) == 4) { set_smem(k_yz<T, l, 1>, sb); set_smem(k_yz<T, l, 1, true>, sb); } break;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Ly");
@@ -854,14 +865,18 @@ void launch_fast_xi(const cx<T>* S, T* h, const Geom& g, const cx<T>* tw, cudaSt
 
 template <typename T>
 void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, StepCtl* ctl,
-                    const StageTable& st, int prologue, cudaStream_t stream, bool pdl) {
+                    const StageTable& st, int prologue, cudaStream_t stream, bool pdl, const RowMap<T>* rows) {
+    RowMap<T> rm{};
+    if (rows) rm = *rows;
     int sb = 0;
     const int kxb = fast_yz_kxb<T>(g, &sb);
     const unsigned grid = static_cast<unsigned>((g.xh + kxb - 1) / kxb);
     switch (g.log2ly) {
 #define X(l) case l: \
-        if (g.nz == 1) launch_pdl(pdl, k_yz<T, l, 0>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue); \
-        else if constexpr (sizeof(T) == 4) launch_pdl(pdl, k_yz<T, l, 1>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue); \
+        if (g.nz == 1) { if (rows) launch_pdl(pdl, k_yz<T, l, 0, true>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); \
+                         else launch_pdl(pdl, k_yz<T, l, 0>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); } \
+        else if constexpr (sizeof(T) == 4) { if (rows) launch_pdl(pdl, k_yz<T, l, 1, true>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); \
+                         else launch_pdl(pdl, k_yz<T, l, 1>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); } \
         else throw std::invalid_argument("fast path: f64 needs nz == 1"); break;
         MMB_FAST_CASES(X)
 #undef X
@@ -912,7 +927,7 @@ void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>
                                     const StageTable&, int, cudaStream_t);                     \
     template void launch_fast_xi<T>(const cx<T>*, T*, const Geom&, const cx<T>*, cudaStream_t); \
     template void launch_fast_yz<T>(cx<T>*, const Geom&, const cx<T>*, const T*, StepCtl*,         \
-                                    const StageTable&, int, cudaStream_t, bool);               \
+                                    const StageTable&, int, cudaStream_t, bool, const RowMap<T>*); \
     template int fast_xstep_blocks<T>(const Geom&);                                            \
     template void launch_fast_xstep<T>(cx<T>*, const T*, T*, const Geom&, const cx<T>*, double, \
                                        double, StepCtl*, double*, cudaStream_t, bool);

@@ -18,10 +18,19 @@
 // one device with device copies instead, which makes the decomposition testable on one GPU:
 // per-rank kernels are the single-device kernels on sub-grids, so the sharded fields equal
 // the single-device ones bitwise.
+//
+// Peer mode (MMB_SHARD_PEER=1): no transposes. The y/z kernels of rank r read the rows of its
+// kx columns straight from every rank's S_loc and write the results back there (RowMap: plain
+// loads/stores into the peers' memory over NVLink, mapped with CUDA IPC), and the halo planes
+// are copied peer to peer. Two stream-ordered barriers (a one-word ncclAllReduce) per step
+// separate the phases: every rank's KXS has written its S_loc before anyone's y/z reads it,
+// and every y/z write-back has landed before any KXS reads. In emulated mode the same kernels
+// run with all S_loc buffers on one device.
 #include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -132,6 +141,12 @@ public:
             std::memcpy(&id, nccl_id, sizeof(id));
             nck(ncclCommInitRank(&comm_, world, id, my_rank), "ncclCommInitRank");
         }
+        const char* pe = std::getenv("MMB_SHARD_PEER");
+        peer_ = pe && pe[0] == '1' && world > 1;
+        if (peer_) {
+            if (world > kMaxRanks) throw std::invalid_argument("mmb: peer mode supports up to 8 ranks");
+            setup_peers();
+        }
         prepare_fast_kernels<T>(ranks_[0]->gs);
         if (yz_) prepare_fast_kernels<T>(ranks_[0]->gc);
         else prepare_big_kernels<T>(ranks_[0]->gc);
@@ -154,6 +169,16 @@ public:
     }
 
     ~ShardSolver() override {
+        if (peer_ && !emulated_) {
+            // nobody frees its buffers while a peer may still read them
+            try {
+                barrier();
+                cudaStreamSynchronize(stream_);
+            } catch (...) {
+            }
+            for (void* p : ipc_open_)
+                if (p) cudaIpcCloseMemHandle(p);
+        }
         if (comm_) ncclCommDestroy(comm_);
         ranks_.clear();
         if (stream_) cudaStreamDestroy(stream_);
@@ -199,6 +224,10 @@ public:
     }
 
     void step(long long n) override {
+        if (peer_) {
+            step_peer(n);
+            return;
+        }
         for (long long i = 0; i < n; ++i) {
             prime();
             transpose_forward();
@@ -354,6 +383,122 @@ public:
     }
 
 private:
+    // ---- peer mode -------------------------------------------------------------------------
+    void step_peer(long long n) {
+        for (long long i = 0; i < n; ++i) {
+            prime();
+            barrier(); // every rank's S_loc (KXS / prime output) is complete
+            for (size_t k = 0; k < ranks_.size(); ++k) {
+                Rank<T>& R = *ranks_[k];
+                const RowMap<T>& rm = rowmaps_[k];
+                if (R.ncols == 0) continue;
+                if (yz_) {
+                    launch_fast_yz<T>(R.s_loc.p, R.gc, R.twy.p, R.kspec.p, R.ctl.p, st_, 1, stream_, false, &rm);
+                } else {
+                    launch_big_yf<T>(R.s_loc.p, R.s2.p, R.gc, R.twy.p, R.ctl.p, st_, 1, stream_, &rm);
+                    launch_big_z<T>(R.s2.p, R.gc, R.twz.p, R.kspec.p, stream_);
+                    launch_big_yi<T>(R.s2.p, R.s_loc.p, R.gc, R.twy.p, stream_, &rm);
+                }
+            }
+            barrier(); // every y/z write-back into the S_loc buffers has landed
+            halo_peer(cur_);
+            for (auto& rp : ranks_) {
+                Rank<T>& R = *rp;
+                launch_fast_xstep<T>(R.s_loc.p, R.m(cur_), R.m(cur_ ^ 1), R.gs, R.twx.p, exch_coeff_,
+                                     aniso_coeff_, R.ctl.p, R.tpart.p, stream_);
+            }
+            cur_ ^= 1;
+            ++step_;
+        }
+    }
+
+    // stream-ordered barrier across ranks (nothing to do when all ranks share one stream)
+    void barrier() {
+        if (emulated_) return;
+        nck(ncclAllReduce(bar_.p, bar_.p, 1, ncclInt32, ncclSum, comm_, stream_), "ncclAllReduce (barrier)");
+    }
+
+    // S_loc and M base pointers of every rank: local buffers in emulated mode, CUDA IPC
+    // mappings of the peers' allocations otherwise (handles all-gathered over NCCL)
+    void setup_peers() {
+        s_loc_of_.assign(world_, nullptr);
+        m_of_[0].assign(world_, nullptr);
+        m_of_[1].assign(world_, nullptr);
+        if (emulated_) {
+            for (auto& rp : ranks_) {
+                s_loc_of_[rp->rank] = rp->s_loc.p;
+                m_of_[0][rp->rank] = rp->mb[0].p;
+                m_of_[1][rp->rank] = rp->mb[1].p;
+            }
+        } else {
+            Rank<T>& R = *ranks_[0];
+            bar_.alloc(1);
+            ck(cudaMemsetAsync(bar_.p, 0, sizeof(int), stream_), "memset");
+            constexpr int H = sizeof(cudaIpcMemHandle_t);
+            std::vector<unsigned char> mine(3 * H), all(static_cast<size_t>(3) * H * world_);
+            void* ptrs[3] = {R.s_loc.p, R.mb[0].p, R.mb[1].p};
+            for (int i = 0; i < 3; ++i) {
+                cudaIpcMemHandle_t h;
+                ck(cudaIpcGetMemHandle(&h, ptrs[i]), "cudaIpcGetMemHandle");
+                std::memcpy(mine.data() + i * H, &h, H);
+            }
+            DevBuf<unsigned char> dall;
+            dall.alloc(all.size());
+            ck(cudaMemcpyAsync(dall.p + static_cast<size_t>(R.rank) * 3 * H, mine.data(), 3 * H, cudaMemcpyHostToDevice,
+                               stream_), "ipc handles");
+            nck(ncclAllGather(dall.p + static_cast<size_t>(R.rank) * 3 * H, dall.p, 3 * H, ncclUint8, comm_, stream_),
+                "ncclAllGather");
+            ck(cudaMemcpyAsync(all.data(), dall.p, all.size(), cudaMemcpyDeviceToHost, stream_), "ipc handles");
+            ck(cudaStreamSynchronize(stream_), "ipc sync");
+            for (int q = 0; q < world_; ++q) {
+                void* p[3] = {ptrs[0], ptrs[1], ptrs[2]};
+                if (q != R.rank) {
+                    for (int i = 0; i < 3; ++i) {
+                        cudaIpcMemHandle_t h;
+                        std::memcpy(&h, all.data() + (static_cast<size_t>(q) * 3 + i) * H, H);
+                        ck(cudaIpcOpenMemHandle(&p[i], h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+                        ipc_open_.push_back(p[i]);
+                    }
+                }
+                s_loc_of_[q] = static_cast<cx<T>*>(p[0]);
+                m_of_[0][q] = static_cast<T*>(p[1]);
+                m_of_[1][q] = static_cast<T*>(p[2]);
+            }
+        }
+        for (auto& rp : ranks_) {
+            RowMap<T> rm{};
+            rm.world = world_;
+            rm.k0 = rp->k0;
+            for (int q = 0; q < world_; ++q) {
+                rm.base[q] = s_loc_of_[q];
+                rm.z0[q] = slabs_[q].first;
+            }
+            rm.z0[world_] = d_.nz;
+            rowmaps_.push_back(rm);
+        }
+    }
+
+    // halo planes of M_cur copied from the neighbours' slabs (peer to peer)
+    void halo_peer(int which) {
+        const size_t plane = static_cast<size_t>(d_.nx) * d_.ny, pb = plane * sizeof(T);
+        for (auto& rp : ranks_) {
+            Rank<T>& R = *rp;
+            for (int c = 0; c < 3; ++c) {
+                T* mc = R.m(which) + c * R.gs.cs;
+                if (R.rank > 0) {
+                    const int q = R.rank - 1, nq = slabs_[q].second - slabs_[q].first;
+                    const T* src = m_of_[which][q] + plane + c * (nq + 2) * plane + (nq - 1) * plane;
+                    ck(cudaMemcpyAsync(mc - plane, src, pb, cudaMemcpyDefault, stream_), "halo (peer)");
+                }
+                if (R.rank + 1 < world_) {
+                    const int q = R.rank + 1, nq = slabs_[q].second - slabs_[q].first;
+                    const T* src = m_of_[which][q] + plane + c * (nq + 2) * plane;
+                    ck(cudaMemcpyAsync(mc + R.nzl * plane, src, pb, cudaMemcpyDefault, stream_), "halo (peer)");
+                }
+            }
+        }
+    }
+
     void set_schedule(const mmb_stage* stages, int n) {
         if (n < 0 || (n > 0 && !stages)) throw std::invalid_argument("mmb: bad stage list");
         if (n > kMaxStages) throw std::invalid_argument("mmb: too many schedule stages (max 16)");
@@ -634,6 +779,12 @@ private:
     std::vector<std::unique_ptr<Rank<T>>> ranks_;
     cudaStream_t stream_ = nullptr;
     ncclComm_t comm_ = nullptr;
+    bool peer_ = false;
+    std::vector<RowMap<T>> rowmaps_;        // per local rank (peer mode)
+    std::vector<cx<T>*> s_loc_of_;          // every rank's S_loc (peer mode)
+    std::vector<T*> m_of_[2];               // every rank's M buffers, halo planes included
+    std::vector<void*> ipc_open_;
+    DevBuf<int> bar_;
     int cur_ = 0;
     bool s_valid_ = false;
     long long step_ = 0;

@@ -153,6 +153,48 @@ def transpose_backward(p: SlabPlan, rank: int, s_cols, group=None):
     return out
 
 
+# ------------------------------------------------------------------ peer-memory mode
+def peer_row(p: SlabPlan, rank: int, kx_local: int, c: int, z: int) -> Tuple[int, int]:
+    """Where row (kx_local, c, z) of rank `rank`'s columns lives in peer mode (MMB_SHARD_PEER,
+    csrc/fast.hpp RowMap::row): (owning rank q, complex-element offset into q's flat
+    S_local [Xh][3][nslab_q][R])."""
+    q = 0
+    while z >= p.slabs[q][1]:
+        q += 1
+    z0 = p.slabs[q][0]
+    k = p.cols[rank][0] + kx_local
+    return q, ((k * 3 + c) * p.nslab(q) + (z - z0)) * p.rows_per_plane()
+
+
+def gather_columns_from_peers(p: SlabPlan, rank: int, s_locals):
+    """The [ncols, 3, nplanes, R] column block of `rank` read row by row from every rank's
+    S_local (s_locals[q], flat or [Xh, 3, nslab_q, R]): what the peer-mode y/z kernels load
+    instead of the transpose_forward output."""
+    import torch
+    flat = [s.reshape(-1) for s in s_locals]
+    R = p.rows_per_plane()
+    nplanes = p.nz if p.axis == "z" else p.ny
+    out = torch.empty((p.ncols(rank), 3, nplanes, R), dtype=flat[0].dtype)
+    for k in range(p.ncols(rank)):
+        for c in range(3):
+            for z in range(nplanes):
+                q, off = peer_row(p, rank, k, c, z)
+                out[k, c, z] = flat[q][off:off + R]
+    return out
+
+
+def scatter_columns_to_peers(p: SlabPlan, rank: int, s_cols, s_locals):
+    """Write `rank`'s processed column rows back into every rank's S_local in place (the
+    peer-mode y/z kernels' stores, replacing transpose_backward)."""
+    flat = [s.reshape(-1) for s in s_locals]
+    R = p.rows_per_plane()
+    for k in range(s_cols.shape[0]):
+        for c in range(3):
+            for z in range(s_cols.shape[2]):
+                q, off = peer_row(p, rank, k, c, z)
+                flat[q][off:off + R] = s_cols[k, c, z]
+
+
 def halo_exchange(p: SlabPlan, rank: int, m_slab, group=None):
     """m_slab: [3, nslab, ...] (slab axis second). Returns (plane_below, plane_above): the
     neighbours' boundary planes of M (None at the open boundary), for the exchange stencil's

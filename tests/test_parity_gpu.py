@@ -369,14 +369,17 @@ def test_reference_side_adapter_runs():
 
 
 # ---------------------------------------------------------------- slab decomposition
+@pytest.mark.parametrize("peer", ["0", "1"])
 @pytest.mark.parametrize("prec", ["f64", "f32"])
 @pytest.mark.parametrize("grid,world", [((40, 24, 9, 2.0), 2), ((40, 24, 9, 2.0), 3),
                                         ((32, 16, 8, 1.0), 2), ((24, 20, 33, 1.5), 4),
-                                        ((16, 12, 4, 2.5), 4)])
-def test_sharded_pipeline_equals_single_device(grid, world, prec, monkeypatch):
-    """The z-slab decomposition (all-to-all transposes, per-rank column y/z kernels, halo
-    exchange, slab KXS) run as `world` emulated ranks on this GPU reproduces the single-device
-    solver on the same path bitwise, through a ramp stage and the sticky alpha override."""
+                                        ((16, 12, 4, 2.5), 4), ((24, 20, 33, 1.5), 8)])
+def test_sharded_pipeline_equals_single_device(grid, world, prec, peer, monkeypatch):
+    """The z-slab decomposition run as `world` emulated ranks on this GPU reproduces the
+    single-device solver on the same path bitwise, through a ramp stage and the sticky alpha
+    override: with all-to-all transposes into column buffers (peer 0), and with the y/z
+    kernels reading and writing every rank's slab spectrum directly (peer 1, RowMap)."""
+    monkeypatch.setenv("MMB_SHARD_PEER", peer)
     from paper_1501_07293_b200 import Precision
     from paper_1501_07293_b200.simulation import make_emulated_sharded_simulation
     nx, ny, nz, delta = grid

@@ -113,3 +113,55 @@ def test_plan_partitions_and_counts():
     b = p.bytes_per_step(4)
     # f32: each rank ships 7/8 of its 1/8 share of the 6.4 GB half spectrum each way
     assert abs(b["transpose_each_way"] - 2049 * 3 * 8 * 2048 * 8 * 7 / 8) < 2049 * 3 * 8 * 2048 * 8
+
+
+def _peer_rank_main(rank, world, port, nx, ny, nz, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = shard.plan(nx, ny, nz, world)
+        gen = torch.Generator().manual_seed(7 + rank)
+        mine = torch.complex(torch.randn(p.xh, 3, p.nslab(rank), ny, generator=gen, dtype=torch.float64),
+                             torch.randn(p.xh, 3, p.nslab(rank), ny, generator=gen, dtype=torch.float64))
+        # every rank's S_local, as the IPC-mapped peer views would show them
+        sizes = [p.xh * 3 * p.nslab(r) * ny for r in range(world)]
+        flat = torch.view_as_real(mine.reshape(-1)).reshape(-1)
+        padded = [torch.empty(2 * max(sizes), dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(padded, torch.nn.functional.pad(flat, (0, 2 * max(sizes) - flat.numel())))
+        locals_ = [torch.view_as_complex(padded[r][:2 * sizes[r]].reshape(-1, 2)).clone() for r in range(world)]
+        cols_t = shard.transpose_forward(p, rank, mine)
+        cols_p = shard.gather_columns_from_peers(p, rank, locals_)
+        ok_fwd = torch.equal(cols_t, cols_p)
+        # write back a transformed block both ways
+        new_cols = cols_t * (2.0 - 1.0j) + 0.5
+        back_t = shard.transpose_backward(p, rank, new_cols)
+        # each rank scatters its own columns into copies of all slabs; gather rank's slab back
+        copies = [l.clone() for l in locals_]
+        obj = [None] * world
+        dist.all_gather_object(obj, new_cols)
+        for r in range(world):
+            shard.scatter_columns_to_peers(p, r, obj[r], copies)
+        ok_bwd = torch.equal(copies[rank].reshape(back_t.shape), back_t)
+        q.put((rank, ok_fwd, ok_bwd))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shape", [(2, (12, 6, 5)), (3, (9, 4, 7))])
+def test_peer_rows_equal_the_transposes(world, shape):
+    """Peer mode (MMB_SHARD_PEER): the rows the y/z kernels read from / write to the peers'
+    slab spectra (RowMap) are exactly the all-to-all transposes' blocks, on world 2 and 3
+    gloo ranks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_rank_main, args=(r, world, port, *shape, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert all(ok_f and ok_b for _, ok_f, ok_b in res), res
