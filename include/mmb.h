@@ -147,7 +147,10 @@ int mmb_device_bytes(mmb_ctx* ctx, size_t* out);
  * effective_field, demag_field, tensor) are single-device only. mmb_create_emulated runs all
  * `world` ranks of the same decomposition on this process's device (exchanges by device
  * copies) and exposes the whole grid — used to test the sharded pipeline on one GPU.
- * With world == 1, mmb_create_sharded returns the single-device solver (nothing to exchange). */
+ * With world == 1, mmb_create_sharded returns the single-device solver (nothing to exchange).
+ * MMB_SHARD_PEER=1 (environment, read at creation) replaces the NCCL all-to-all transposes by
+ * y/z kernels that read and write every rank's slab spectrum in place through CUDA IPC
+ * mappings (peer memory over NVLink); see DESIGN.md §6. */
 int mmb_nccl_unique_id(unsigned char out[128]);
 int mmb_create_sharded(const mmb_desc* desc, const mmb_stage* stages, int nstages, int rank,
                        int world, const unsigned char nccl_id[128], mmb_ctx** out);
