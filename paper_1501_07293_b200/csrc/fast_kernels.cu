@@ -795,11 +795,14 @@ int fast_yz_kxb(const Geom& g, int* smem_bytes) {
     const int twb = g.ly * static_cast<int>(sizeof(cx<T>));
     const int limit = 227 * 1024 - twb;
     if (per_kx > limit) return 0;
-    // as many kx per CTA as ~100 KB allows, but never fewer than ~2 CTAs per SM of work
-    int kxb = (100 * 1024) / per_kx;
-    if (kxb < 1) kxb = 1;
-    kxb = std::min(kxb, 64);
-    kxb = std::min(kxb, std::max(1, g.xh / (2 * 148)));
+    // kx per CTA: as many as ~100 KB allows, but no more than ~2 CTAs per SM of work on large
+    // grids, and on small grids enough that the columns fit one CTA wave per SM (measured:
+    // 256x256 films 21.1 -> 16.8 us/step with 2 columns per CTA instead of 1)
+    const int cap = std::max(1, std::min(64, (100 * 1024) / per_kx));
+    int kxb = std::min(cap, std::max(1, g.xh / (2 * 148)));
+    kxb = std::max(kxb, std::min(cap, (g.xh + 147) / 148));
+    if (const char* e = std::getenv("MMB_YZ_KXB"); e && std::atoi(e) > 0) // tuning experiments
+        kxb = std::max(1, std::min(std::atoi(e), cap));
     if (smem_bytes) *smem_bytes = kxb * per_kx + twb;
     return kxb;
 }
