@@ -36,6 +36,10 @@ WORKLOADS = {
     "256x256x1_f32": (256, 256, 1, 3.0, 1.3e7, 800.0, 0.0, 0.5, 5e-6, "f32"),
     "256x256x1_f64": (256, 256, 1, 3.0, 1.3e7, 800.0, 0.0, 0.5, 5e-6, "f64"),
     "sp4_128x32x1_f64": (128, 32, 1, 3.90625, 1.3e7, 800.0, 0.0, 0.5, 5e-6, "f64"),
+    # the reference's own benchmark verb: SP#3 cube relaxation n^3 (proj/src/benchmark.cpp)
+    "sp3_64_f32": (64, 64, 64, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5, "f32"),
+    "sp3_64_f64": (64, 64, 64, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5, "f64"),
+    "sp3_128_f32": (128, 128, 128, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5, "f32"),
     # BASELINE configs[4]: slab-sharded across the GPUs of the box (strong scaling)
     "2048x2048x64_f32": (2048, 2048, 64, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5, "f32"),
 }

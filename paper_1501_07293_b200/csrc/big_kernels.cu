@@ -127,9 +127,9 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
 
 // z pencils: W consecutive ky of one kx, all three components, Lz = 2^LOG2LZ >= 2 nz - 1.
 // pencils per CTA: 32 (f32) keeps the tile at 98 KB (two CTAs per SM) up to Lz = 64; the
-// Lz = 128 tile halves it for the same occupancy
+// Lz = 128 and 256 tiles halve / quarter it for the same occupancy
 template <typename T, int LOG2LZ>
-constexpr int zw() { return (sizeof(T) == 4 ? 32 : 16) >> (LOG2LZ >= 7 ? 1 : 0); }
+constexpr int zw() { return (sizeof(T) == 4 ? 32 : 16) >> (LOG2LZ >= 8 ? 2 : (LOG2LZ >= 7 ? 1 : 0)); }
 constexpr int kZThreads = 256;
 template <typename T, int LOG2LZ>
 constexpr int z_smem_bytes() {
@@ -215,10 +215,13 @@ __global__ void __launch_bounds__(kZThreads)
         const bool fy = 2 * ky > ly;
         const int kyo = fy ? ly - ky : ky;
         const T* kb = kt + (static_cast<long long>(kx) * zh * yh + kyo) * 6;
-        T k6[N1][6];
-        if (w < wl) {
+        // (f64 at Lz = 256: the 16 coefficient sets would spill, so they are loaded next to
+        // their use there)
+        constexpr bool PREF = N1 <= 8 || sizeof(T) == 4;
+        T k6[PREF ? N1 : 1][6];
+        if (PREF && w < wl) {
 #pragma unroll
-            for (int k1 = 0; k1 < N1; ++k1) {
+            for (int k1 = 0; k1 < (PREF ? N1 : 0); ++k1) {
                 const int kz = k2 + N2 * k1;
                 const int kzo = 2 * kz > LZ ? LZ - kz : kz;
                 load6<T>(kb + static_cast<long long>(kzo) * yh * 6, k6[k1]);
@@ -237,10 +240,12 @@ __global__ void __launch_bounds__(kZThreads)
             for (int k1 = 0; k1 < N1; ++k1) {
                 const int kz = k2 + N2 * k1;
                 const bool fz = 2 * kz > LZ;
-                if (fy) k6[k1][1] = -k6[k1][1];
-                if (fz) k6[k1][2] = -k6[k1][2];
-                if (fy != fz) k6[k1][4] = -k6[k1][4];
-                mac3<T>(k6[k1], u[0][k1], u[1][k1], u[2][k1]);
+                T(&kk)[6] = k6[PREF ? k1 : 0];
+                if constexpr (!PREF) load6<T>(kb + static_cast<long long>(fz ? LZ - kz : kz) * yh * 6, k6[0]);
+                if (fy) kk[1] = -kk[1];
+                if (fz) kk[2] = -kk[2];
+                if (fy != fz) kk[4] = -kk[4];
+                mac3<T>(kk, u[0][k1], u[1][k1], u[2][k1]);
             }
         }
 #pragma unroll
@@ -285,14 +290,14 @@ void set_smem(K kernel, int bytes) {
 }
 
 #define MMB_Y_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12)
-#define MMB_Z_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7)
+#define MMB_Z_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
 
 } // namespace
 
 template <typename T>
 bool big_supported(const Geom& g) {
     if (g.lx < 2 || g.ly < 2 || g.nz < 2) return false;
-    if (g.log2lx > 12 || g.log2ly > 12 || g.log2lz > 7) return false;
+    if (g.log2lx > 12 || g.log2ly > 12 || g.log2lz > 8) return false;
     if (sizeof(T) == 8 && (g.log2lx > 10 || g.log2ly > 10)) return false; // DFT_64 f64 spills
     return true;
 }

@@ -68,6 +68,46 @@ def test_demag_field_matches_reference(refsolver, grid, prec, path):
     assert rel(sim.demag_field(m), want) <= TOL_H[prec]
 
 
+def _symmetrized_reference_field(t, m, nx, ny, nz):
+    """The reference's zero-padded 2n FFT convolution (demag.cpp:53-147, in NumPy) on its own
+    tensor made exactly symmetric: negative offsets take the parity image of the computed
+    non-negative octant, as in the B200 wrapped real spectrum."""
+    oc = octant_from_shifted(t, nx, ny, nz)
+    odd = {0: (0, 0, 0), 1: (1, 1, 0), 2: (1, 0, 1), 3: (0, 0, 0), 4: (0, 1, 1), 5: (0, 0, 0)}
+    ts = np.zeros_like(t)
+    for c in range(6):
+        for sz in (1, -1):
+            for sy in (1, -1):
+                for sx in (1, -1):
+                    sgn = (sx if odd[c][0] else 1) * (sy if odd[c][1] else 1) * (sz if odd[c][2] else 1)
+                    idx = np.ix_(nz - 1 + sz * np.arange(nz), ny - 1 + sy * np.arange(ny), nx - 1 + sx * np.arange(nx))
+                    ts[c][idx] = sgn * oc[c]
+    K = [np.fft.fftn(np.roll(ts[c], (-(nz - 1), -(ny - 1), -(nx - 1)), axis=(0, 1, 2))) for c in range(6)]
+    Mh = [np.fft.fftn(np.pad(m[i].astype(np.float64), ((0, nz), (0, ny), (0, nx)))) for i in range(3)]
+    xx, xy, xz, yy, yz, zz = K
+    H = [xx * Mh[0] + xy * Mh[1] + xz * Mh[2], xy * Mh[0] + yy * Mh[1] + yz * Mh[2], xz * Mh[0] + yz * Mh[1] + zz * Mh[2]]
+    return np.stack([np.fft.ifftn(h).real[:nz, :ny, :nx] for h in H])
+
+
+@pytest.mark.parametrize("grid", [(8, 6, 70, 1.0), (70, 6, 8, 1.0)])
+def test_long_column_demag_and_tensor_symmetry(refsolver, grid, path):
+    """Lz = 256 (the z-stage's largest size) and a long x column. The reference computes the
+    tensor at negative offsets separately, so its tensor is symmetric only up to rounding of
+    the O(1) corner terms; on these ~3000-cell grids that asymmetry alone moves H by 1.1e-12 /
+    2.0e-12 relative (the reference's FFT vs its own direct sum agrees to 4e-15). The B200
+    wrapped real spectrum is exactly symmetric: against the reference's convolution fed its own
+    tensor symmetrized it agrees to 1e-13, and against the reference itself to 2.5e-12."""
+    nx, ny, nz, delta = grid
+    sp = spec(nx, ny, nz, delta)
+    sim = b200(sp, "f64")
+    m = refsolver.random_unit_field(nx, ny, nz, 800.0, 20240 + nx, np.float64)
+    got = sim.demag_field(m)
+    want = refsolver.heff(ref_problem(refsolver, sp), m, parts=1)
+    assert rel(got, want) <= 2.5e-12
+    sym = _symmetrized_reference_field(refsolver.build_tensor(nx, ny, nz, delta), m, nx, ny, nz)
+    assert rel(got, sym) <= 1e-13
+
+
 @pytest.mark.parametrize("prec", ["f64", "f32"])
 def test_demag_fft_vs_direct_sum(refsolver, prec):
     # proj/tests/test_demag_field.cpp:150-172 criterion on the B200 path
