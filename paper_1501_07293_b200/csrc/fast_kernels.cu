@@ -217,20 +217,22 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
 }
 
 // ------------------------------------------------------------------ KYZ: y, z, MAC, z^-1, y^-1
-template <int LOG2L>
+template <typename T, int LOG2L>
 constexpr int yz_threads() {
-    constexpr int n2 = Split<LOG2L>::N2;
-    return n2 >= 384 ? n2 : (384 / n2) * n2;
+    // f32: ~384 threads; f64: ~192 so the DFT registers (2 per complex component) fit without
+    // spilling under the launch bound
+    constexpr int n2 = Split<LOG2L>::N2, target = sizeof(T) == 8 ? 192 : 384;
+    return n2 >= target ? n2 : (target / n2) * n2;
 }
 
 template <typename T, int LOG2L, int ZM, bool PEER = false>
-__global__ void __launch_bounds__(yz_threads<LOG2L>())
+__global__ void __launch_bounds__(yz_threads<T, LOG2L>())
     k_yz(cx<T>* __restrict__ S, Geom g, const cx<T>* __restrict__ tw, const T* __restrict__ kt,
          int kxb, StepCtl* ctl, StageTable st, int prologue, RowMap<T> rm) {
     using SP = Split<LOG2L>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2;
     constexpr int RP = fpitch<LOG2L>();
-    constexpr int NT = yz_threads<LOG2L>();
+    constexpr int NT = yz_threads<T, LOG2L>();
     constexpr int RB = NT / N2; // rows per batch
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
@@ -477,9 +479,10 @@ dim3 xs_grid(const Geom& g) {
 
 template <typename T, int LOG2L, int PB>
 constexpr int xs_min_blocks() {
-    // two or three CTAs per SM when their shared memory fits (registers capped accordingly)
+    // two or three CTAs per SM when their shared memory fits (registers capped accordingly;
+    // f64 tiles keep at most two so their DFT registers do not spill)
     constexpr int b = xs_smem_bytes<T, LOG2L, PB>() + 2048;
-    return (XS<LOG2L, PB>::NT <= 256 && 3 * b <= 228 * 1024) ? 3 : (2 * b <= 228 * 1024 ? 2 : 1);
+    return (sizeof(T) == 4 && XS<LOG2L, PB>::NT <= 256 && 3 * b <= 228 * 1024) ? 3 : (2 * b <= 228 * 1024 ? 2 : 1);
 }
 
 // PB = 128: ~384 threads and 3 x 8 rows per CTA (large grids); PB = 16: 3 x 2 rows for
@@ -876,10 +879,10 @@ void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, StepC
     const unsigned grid = static_cast<unsigned>((g.xh + kxb - 1) / kxb);
     switch (g.log2ly) {
 #define X(l) case l: \
-        if (g.nz == 1) { if (rows) launch_pdl(pdl, k_yz<T, l, 0, true>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); \
-                         else launch_pdl(pdl, k_yz<T, l, 0>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); } \
-        else if constexpr (sizeof(T) == 4) { if (rows) launch_pdl(pdl, k_yz<T, l, 1, true>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); \
-                         else launch_pdl(pdl, k_yz<T, l, 1>, grid, yz_threads<l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); } \
+        if (g.nz == 1) { if (rows) launch_pdl(pdl, k_yz<T, l, 0, true>, grid, yz_threads<T, l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); \
+                         else launch_pdl(pdl, k_yz<T, l, 0>, grid, yz_threads<T, l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); } \
+        else if constexpr (sizeof(T) == 4) { if (rows) launch_pdl(pdl, k_yz<T, l, 1, true>, grid, yz_threads<T, l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); \
+                         else launch_pdl(pdl, k_yz<T, l, 1>, grid, yz_threads<T, l>(), sb, stream, S, g, tw, kt, kxb, ctl, st, prologue, rm); } \
         else throw std::invalid_argument("fast path: f64 needs nz == 1"); break;
         MMB_FAST_CASES(X)
 #undef X
