@@ -48,7 +48,7 @@ template <typename T, int LOG2L, int INV, bool PEER = false>
 __global__ void __launch_bounds__(YR<LOG2L>::NT)
     k_yrow(const cx<T>* __restrict__ in, cx<T>* __restrict__ out, long long nrows, int in_pitch,
            int out_pitch, int n_live, const cx<T>* __restrict__ tw, StepCtl* ctl, StageTable st,
-           int prologue, RowMap<T> rm, int nzr) {
+           int prologue, const __grid_constant__ RowMap<T> rm, int nzr) {
     using SP = Split<LOG2L>;
     using Y = YR<LOG2L>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = Y::P, EX = Y::EX, NT = Y::NT;

@@ -219,16 +219,16 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
 // ------------------------------------------------------------------ KYZ: y, z, MAC, z^-1, y^-1
 template <typename T, int LOG2L>
 constexpr int yz_threads() {
-    // f32: ~384 threads; f64: ~192 so the DFT registers (2 per complex component) fit without
-    // spilling under the launch bound
-    constexpr int n2 = Split<LOG2L>::N2, target = sizeof(T) == 8 ? 192 : 384;
+    // ~384 threads; ~192 for f64 and for DFT_64 stages, so the stage-A registers fit under the
+    // launch bound without spilling
+    constexpr int n2 = Split<LOG2L>::N2, target = (sizeof(T) == 8 || n2 >= 64) ? 192 : 384;
     return n2 >= target ? n2 : (target / n2) * n2;
 }
 
 template <typename T, int LOG2L, int ZM, bool PEER = false>
 __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
     k_yz(cx<T>* __restrict__ S, Geom g, const cx<T>* __restrict__ tw, const T* __restrict__ kt,
-         int kxb, StepCtl* ctl, StageTable st, int prologue, RowMap<T> rm) {
+         int kxb, StepCtl* ctl, StageTable st, int prologue, const __grid_constant__ RowMap<T> rm) {
     using SP = Split<LOG2L>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2;
     constexpr int RP = fpitch<LOG2L>();
@@ -482,7 +482,8 @@ constexpr int xs_min_blocks() {
     // two or three CTAs per SM when their shared memory fits (registers capped accordingly;
     // f64 tiles keep at most two so their DFT registers do not spill)
     constexpr int b = xs_smem_bytes<T, LOG2L, PB>() + 2048;
-    return (sizeof(T) == 4 && XS<LOG2L, PB>::NT <= 256 && 3 * b <= 228 * 1024) ? 3 : (2 * b <= 228 * 1024 ? 2 : 1);
+    return (sizeof(T) == 4 && LOG2L <= 9 && XS<LOG2L, PB>::NT <= 256 && 3 * b <= 228 * 1024)
+               ? 3 : (2 * b <= 228 * 1024 ? 2 : 1);
 }
 
 // PB = 128: ~384 threads and 3 x 8 rows per CTA (large grids); PB = 16: 3 x 2 rows for
