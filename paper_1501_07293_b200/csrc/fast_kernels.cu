@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
 //   3. x-r2c of the new tile -> the half spectra S for the next step, in place.
 // H_demag never reaches HBM and M_{t+1} is not re-read: per step the x side moves
 // S in + S out + M_t + M_{t+1} instead of three separate passes.
-template <int LOG2L, int PB = 128>
+template <int LOG2L, int PB = 128, int TSIZE = 4>
 struct XS {
     using SP = Split<LOG2L>;
     // Lx = 4096 halves the tile so exchange buffer + twiddle table stay within 227 KB
@@ -456,7 +456,8 @@ struct XS {
 #ifndef MMB_XS_TM_THREADS
 #define MMB_XS_TM_THREADS 192
 #endif
-    static constexpr int TM = (PB <= 16 && LA == 1 && LB == 1 && NT0 < MMB_XS_TM_THREADS) ? MMB_XS_TM_THREADS / NT0 : 1;
+    static constexpr int TM = ((TSIZE == 4 || LOG2L <= 8) && PB <= 16 && LA == 1 && LB == 1 && NT0 < MMB_XS_TM_THREADS)
+                                  ? MMB_XS_TM_THREADS / NT0 : 1; // (f64 above Lx = 256: the registers limit)
     static constexpr int NT = NT0 * TM;                                         // threads
     static_assert(P * SP::N1 * LA <= NT0 && P * SP::N2 * LB == NT0 * RB, "stage tasks");
     static_assert(TM == 1 || (LA == 1 && LB == 1), "pair shuffles need every lane");
@@ -468,7 +469,7 @@ struct XS {
 };
 template <typename T, int LOG2L, int PB>
 constexpr int xs_smem_bytes() {
-    return (XS<LOG2L, PB>::AREA + (1 << LOG2L)) * static_cast<int>(sizeof(cx<T>));
+    return (XS<LOG2L, PB, sizeof(T)>::AREA + (1 << LOG2L)) * static_cast<int>(sizeof(cx<T>));
 }
 
 template <typename X>
@@ -482,18 +483,18 @@ constexpr int xs_min_blocks() {
     // two or three CTAs per SM when their shared memory fits (registers capped accordingly;
     // f64 tiles keep at most two so their DFT registers do not spill)
     constexpr int b = xs_smem_bytes<T, LOG2L, PB>() + 2048;
-    return (sizeof(T) == 4 && LOG2L <= 9 && XS<LOG2L, PB>::NT <= 256 && 3 * b <= 228 * 1024)
+    return (sizeof(T) == 4 && LOG2L <= 9 && XS<LOG2L, PB, sizeof(T)>::NT <= 256 && 3 * b <= 228 * 1024)
                ? 3 : (2 * b <= 228 * 1024 ? 2 : 1);
 }
 
 // PB = 128: ~384 threads and 3 x 8 rows per CTA (large grids); PB = 16: 3 x 2 rows for
 // grids whose row count would otherwise leave SMs idle.
 template <typename T, int LOG2L, int PB>
-__global__ void __launch_bounds__(XS<LOG2L, PB>::NT, xs_min_blocks<T, LOG2L, PB>())
+__global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T, LOG2L, PB>())
     k_xstep(cx<T>* __restrict__ S, const T* __restrict__ m, T* __restrict__ mout, Geom g,
             const cx<T>* __restrict__ tw, T coeff, T kan, StepCtl* ctl, double* __restrict__ tpart) {
     using SP = Split<LOG2L>;
-    using X = XS<LOG2L, PB>;
+    using X = XS<LOG2L, PB, sizeof(T)>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = X::P, TR = X::TR, NT = X::NT;
     constexpr int XH = L / 2 + 1, XHP = X::XHP, EX = X::EX, ZP = X::ZP;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -915,10 +916,10 @@ void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>
     const T coeff = static_cast<T>(exch_coeff), kan = static_cast<T>(aniso_coeff);
     switch (g.log2lx) {
 #define X(l) case l: if (xstep_small<l>(g)) { const dim3 grid = xs_grid<XS<l, 16>>(g); \
-        launch_pdl(pdl, k_xstep<T, l, 16>, grid, XS<l, 16>::NT, xs_smem_bytes<T, l, 16>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); \
+        launch_pdl(pdl, k_xstep<T, l, 16>, grid, XS<l, 16, sizeof(T)>::NT, xs_smem_bytes<T, l, 16>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); \
         } else { if (xs_smem_bytes<T, l, MMB_XS_PB>() > 227 * 1024) throw std::invalid_argument("fast path: x tile exceeds shared memory"); \
         const dim3 grid = xs_grid<XS<l, MMB_XS_PB>>(g); \
-        launch_pdl(pdl, k_xstep<T, l, MMB_XS_PB>, grid, XS<l, MMB_XS_PB>::NT, xs_smem_bytes<T, l, MMB_XS_PB>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
+        launch_pdl(pdl, k_xstep<T, l, MMB_XS_PB>, grid, XS<l, MMB_XS_PB, sizeof(T)>::NT, xs_smem_bytes<T, l, MMB_XS_PB>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");
