@@ -116,7 +116,9 @@ public:
         if (fast_) prepare_fast_kernels<T>(g_);
         else prepare_fft_kernels<T>(g_);
         if (fast_ && !yz_) prepare_big_kernels<T>(g_);
-        pdl_ = g.n >= (1LL << 20);
+        // PDL pays on multi-wave grids (>= 1 M cells) and on SP#4-size grids (a few thousand
+        // cells, launch-latency bound); on mid-size films it costs time
+        pdl_ = g.n >= (1LL << 20) || g.n <= 8192;
         if (const char* e = std::getenv("MMB_PDL"); e && e[0] == '1') pdl_ = true; // tuning
         if (const char* v = std::getenv("MMB_VERBOSE"); v && v[0] == '1')
             std::fprintf(stderr, "mmb: %dx%dx%d L=%dx%dx%d path=%s\n", d.nx, d.ny, d.nz, g.lx, g.ly, g.lz,
