@@ -475,7 +475,9 @@ constexpr int xs_smem_bytes() {
 template <typename X>
 dim3 xs_grid(const Geom& g) {
     const unsigned tiles = static_cast<unsigned>((g.ny + X::TR - 1) / X::TR);
-    return X::ZFAST ? dim3(g.nz, tiles) : dim3(tiles, g.nz);
+    if (X::ZFAST) return dim3(g.nz, tiles);
+    const unsigned zc = static_cast<unsigned>(std::min(4, g.nz));
+    return dim3(zc * tiles, (g.nz + zc - 1) / zc);
 }
 
 template <typename T, int LOG2L, int PB>
@@ -504,16 +506,22 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
 
     // ZFAST (tiles of >= 4 rows): z fastest in the grid, so the CTAs of one y tile in
     // neighbouring planes run together and the +-z neighbour rows of the local terms come from
-    // L2 instead of DRAM re-reads. Narrower tiles keep y fastest: their 16-byte row segments
-    // of S share 32-byte sectors with the next tile, which must then run alongside.
-    const int z = X::ZFAST ? blockIdx.x : blockIdx.y;
-    const int y0 = (X::ZFAST ? blockIdx.y : blockIdx.x) * TR;
+    // L2 instead of DRAM re-reads. Narrower tiles go by chunks of 4 planes, z fastest inside a
+    // chunk and y next: neighbouring y tiles (their 16-byte row segments of S share 32-byte
+    // sectors) still run alongside, and only chunk-boundary planes are re-read from DRAM.
+    const int zcn = min(4, g.nz);
+    const int z = X::ZFAST ? blockIdx.x : blockIdx.y * zcn + blockIdx.x % zcn;
+    const int y0 = (X::ZFAST ? blockIdx.y : blockIdx.x / zcn) * TR;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
     const long long cs = g.cs;
     const int zg = g.z0 + z, nzg = g.nz_g;
     const int tid = threadIdx.x;
     pdl_wait();
     pdl_trigger(); // after the wait: at most one kernel ahead of the running one
+    if (!X::ZFAST && z >= g.nz) { // the last chunk's missing planes
+        if (tid == 0) tpart[blockIdx.y * gridDim.x + blockIdx.x] = 0.0;
+        return;
+    }
     const long long cur_step = ctl->cur_step;
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->step = cur_step + 1;
 
@@ -901,8 +909,8 @@ bool xstep_small(const Geom& g) {
 template <typename T>
 int fast_xstep_blocks(const Geom& g) {
     switch (g.log2lx) {
-#define X(l) case l: return xstep_small<l>(g) ? ((g.ny + XS<l, 16>::TR - 1) / XS<l, 16>::TR) * g.nz \
-                                              : ((g.ny + XS<l, MMB_XS_PB>::TR - 1) / XS<l, MMB_XS_PB>::TR) * g.nz;
+#define X(l) case l: { const dim3 gr = xstep_small<l>(g) ? xs_grid<XS<l, 16>>(g) : xs_grid<XS<l, MMB_XS_PB>>(g); \
+        return static_cast<int>(gr.x * gr.y); }
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");
