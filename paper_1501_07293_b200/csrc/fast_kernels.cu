@@ -21,6 +21,10 @@
 #include "llg_cell.cuh"
 #include "fast_common.cuh"
 
+#ifndef MMB_XS_ZC
+#define MMB_XS_ZC 4 // planes per chunk of the 2-row-tile x grid
+#endif
+
 namespace mmb {
 
 namespace {
@@ -476,7 +480,7 @@ template <typename X>
 dim3 xs_grid(const Geom& g) {
     const unsigned tiles = static_cast<unsigned>((g.ny + X::TR - 1) / X::TR);
     if (X::ZFAST) return dim3(g.nz, tiles);
-    const unsigned zc = static_cast<unsigned>(std::min(4, g.nz));
+    const unsigned zc = static_cast<unsigned>(std::min(MMB_XS_ZC, g.nz));
     return dim3(zc * tiles, (g.nz + zc - 1) / zc);
 }
 
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     // L2 instead of DRAM re-reads. Narrower tiles go by chunks of 4 planes, z fastest inside a
     // chunk and y next: neighbouring y tiles (their 16-byte row segments of S share 32-byte
     // sectors) still run alongside, and only chunk-boundary planes are re-read from DRAM.
-    const int zcn = min(4, g.nz);
+    const int zcn = min(MMB_XS_ZC, g.nz);
     const int z = X::ZFAST ? blockIdx.x : blockIdx.y * zcn + blockIdx.x % zcn;
     const int y0 = (X::ZFAST ? blockIdx.y : blockIdx.x / zcn) * TR;
     const int nx = g.nx, ny = g.ny, nz = g.nz;
