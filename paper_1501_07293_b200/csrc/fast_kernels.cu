@@ -790,6 +790,11 @@ void set_smem(K kernel, int bytes) {
 #ifndef MMB_XS_PB
 #define MMB_XS_PB 128 // KXS tile: 3 * (PB / N2) row pairs (XS)
 #endif
+#ifndef MMB_XS_PB10
+#define MMB_XS_PB10 224 // Lx = 1024: 3 x 14 rows at one CTA per SM (37 tiles = exactly 2 waves
+                        // at 512 x 512 x 8; 78.2 -> 74.6 us, with PDL off for this tile)
+#endif
+constexpr int xs_pb(int log2l) { return log2l == 10 ? MMB_XS_PB10 : MMB_XS_PB; }
 
 #define MMB_FAST_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12)
 
@@ -839,7 +844,7 @@ template <typename T>
 void prepare_fast_kernels(const Geom& g) {
     switch (g.log2lx) {
 #define X(l) case l: set_smem(k_xf<T, l>, x_smem_bytes<T, l>()); set_smem(k_xi<T, l>, x_smem_bytes<T, l>()); \
-                     if (xs_smem_bytes<T, l, MMB_XS_PB>() <= 227 * 1024) set_smem(k_xstep<T, l, MMB_XS_PB>, xs_smem_bytes<T, l, MMB_XS_PB>()); \
+                     if (xs_smem_bytes<T, l, xs_pb(l)>() <= 227 * 1024) set_smem(k_xstep<T, l, xs_pb(l)>, xs_smem_bytes<T, l, xs_pb(l)>()); \
                      set_smem(k_xstep<T, l, 16>, xs_smem_bytes<T, l, 16>()); break;
         MMB_FAST_CASES(X)
 #undef X
@@ -907,13 +912,13 @@ void launch_fast_yz(cx<T>* S, const Geom& g, const cx<T>* tw, const T* kt, StepC
 
 template <int LOG2L>
 bool xstep_small(const Geom& g) {
-    return ((g.ny + XS<LOG2L, MMB_XS_PB>::TR - 1) / XS<LOG2L, MMB_XS_PB>::TR) * g.nz < 2 * 148;
+    return ((g.ny + XS<LOG2L, xs_pb(LOG2L)>::TR - 1) / XS<LOG2L, xs_pb(LOG2L)>::TR) * g.nz < 2 * 148;
 }
 
 template <typename T>
 int fast_xstep_blocks(const Geom& g) {
     switch (g.log2lx) {
-#define X(l) case l: { const dim3 gr = xstep_small<l>(g) ? xs_grid<XS<l, 16>>(g) : xs_grid<XS<l, MMB_XS_PB>>(g); \
+#define X(l) case l: { const dim3 gr = xstep_small<l>(g) ? xs_grid<XS<l, 16>>(g) : xs_grid<XS<l, xs_pb(l)>>(g); \
         return static_cast<int>(gr.x * gr.y); }
         MMB_FAST_CASES(X)
 #undef X
@@ -929,9 +934,9 @@ void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>
     switch (g.log2lx) {
 #define X(l) case l: if (xstep_small<l>(g)) { const dim3 grid = xs_grid<XS<l, 16>>(g); \
         launch_pdl(pdl, k_xstep<T, l, 16>, grid, XS<l, 16, sizeof(T)>::NT, xs_smem_bytes<T, l, 16>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); \
-        } else { if (xs_smem_bytes<T, l, MMB_XS_PB>() > 227 * 1024) throw std::invalid_argument("fast path: x tile exceeds shared memory"); \
-        const dim3 grid = xs_grid<XS<l, MMB_XS_PB>>(g); \
-        launch_pdl(pdl, k_xstep<T, l, MMB_XS_PB>, grid, XS<l, MMB_XS_PB, sizeof(T)>::NT, xs_smem_bytes<T, l, MMB_XS_PB>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
+        } else { if (xs_smem_bytes<T, l, xs_pb(l)>() > 227 * 1024) throw std::invalid_argument("fast path: x tile exceeds shared memory"); \
+        const dim3 grid = xs_grid<XS<l, xs_pb(l)>>(g); \
+        launch_pdl(pdl, k_xstep<T, l, xs_pb(l)>, grid, XS<l, xs_pb(l), sizeof(T)>::NT, xs_smem_bytes<T, l, xs_pb(l)>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");

@@ -119,6 +119,9 @@ public:
         // PDL pays on multi-wave grids (>= 1 M cells) and on SP#4-size grids (a few thousand
         // cells, launch-latency bound); on mid-size films it costs time
         pdl_ = g.n >= (1LL << 20) || g.n <= 8192;
+        // ... except with the one-CTA-per-SM Lx = 1024 x tile, whose early-launched CTAs only
+        // get in the way (+4 us at 512 x 512 x 8)
+        if (fast_ && yz_ && g.lx == 1024) pdl_ = false;
         if (const char* e = std::getenv("MMB_PDL"); e && e[0] == '1') pdl_ = true; // tuning
         if (const char* v = std::getenv("MMB_VERBOSE"); v && v[0] == '1')
             std::fprintf(stderr, "mmb: %dx%dx%d L=%dx%dx%d path=%s\n", d.nx, d.ny, d.nz, g.lx, g.ly, g.lz,
