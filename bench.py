@@ -200,12 +200,14 @@ def profile_summary(workload):
 def cpu_reference_time(wl, steps_max, budget_s, warmup=1):
     """Reference Simulation<T>::step() (oracle/_ref) on the host cores, timed like
     proj/src/benchmark.cpp:40-46 (steady clock, warm-up then measured steps)."""
+    # every host thread (torchrun exports OMP_NUM_THREADS=1 per rank; only rank 0 runs this, and
+    # libgomp reads the variable when the reference library loads it below)
+    cores = int(os.environ.get("MMB_REF_THREADS", len(os.sched_getaffinity(0))))
+    os.environ["OMP_NUM_THREADS"] = str(cores)
     from oracle import ref
     nx, ny, nz, delta, a_ex, ms, hk, alpha, dt, prec = WORKLOADS[wl]
     if not ref.available():
         raise RuntimeError("oracle/_ref/libmmsim_ref.so missing (build with make -C oracle)")
-    cores = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     P = ref.Problem(nx, ny, nz, delta, a_ex, ms, hk, alpha, dt)
     t0 = time.perf_counter()
     sim = ref.RefSimulation(P, prec, backend="parallel")
