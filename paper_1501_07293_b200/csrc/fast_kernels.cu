@@ -225,7 +225,10 @@ template <typename T, int LOG2L>
 constexpr int yz_threads() {
     // ~384 threads; ~192 for f64 and for DFT_64 stages, so the stage-A registers fit under the
     // launch bound without spilling
-    constexpr int n2 = Split<LOG2L>::N2, target = (sizeof(T) == 8 || n2 >= 64) ? 192 : 384;
+#ifndef MMB_YZ_NT
+#define MMB_YZ_NT 384
+#endif
+    constexpr int n2 = Split<LOG2L>::N2, target = (sizeof(T) == 8 || n2 >= 64) ? 192 : MMB_YZ_NT;
     return n2 >= target ? n2 : (target / n2) * n2;
 }
 
