@@ -5,9 +5,13 @@ star's target configuration; SP#3 material, random initial state, no applied fie
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload ...]
 
-One process per GPU (torchrun for N > 1). The 512x512x8 grid fits one GPU, so N > 1 runs N
-independent replicas ("replicas only", scaling "weak"); time = max over ranks of the
-CUDA-event time of K steps; value = total cell-updates of all ranks / that time.
+One process per GPU (torchrun for N > 1). N = 1 runs the 512x512x8 f32 headline; N > 1 runs
+BASELINE configs[4], 2048x2048x64 f32 split into z-slabs over the ranks (NCCL all-to-all
+transposes + halo; scaling "strong"), unless --workload picks another grid (grids that fit one
+GPU then run as N independent replicas, scaling "weak"). Time = max over ranks of the
+CUDA-event time of K graph-replayed steps; value = cell-updates of the whole job / that time.
+Initial state: the reference generator (random_unit_field, proj/src/validate.cpp:21-39,
+seed 20240 + nx) via libmmb.so's host utility.
 --impl reference times the reference's own CPU solver (oracle/_ref: the reference sources
 compiled in place with the FFTW-API shim) on the host cores, rank 0 only.
 Prints one JSON line on rank 0.
@@ -180,11 +184,46 @@ def sum_over_ranks(world, v):
     return float(t.item())
 
 
-def random_state(nx, ny, nz, ms, dtype, seed=20240):
-    rng = np.random.default_rng(seed + nx)
-    v = rng.uniform(-1.0, 1.0, (3, nz, ny, nx))
-    v /= np.maximum(np.sqrt((v * v).sum(0)), 0.1)
-    return (ms * v).astype(dtype)
+def random_state(nx, ny, nz, ms, prec, z0=0, nz_local=None):
+    """The reference generator's field (seed 20240 + nx), planes
+    [z0, z0 + nz_local), from libmmb.so's host utility mmb_random_unit_field."""
+    from paper_1501_07293_b200 import Precision, random_unit_field
+    return random_unit_field(nx, ny, nz, ms, 20240 + nx, Precision.f32 if prec == "f32" else Precision.f64,
+                             z0=z0, nz_local=nz_local)
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def pcie_copy_ms(nbytes, dtype):
+    """Device time of one pinned H2D plus one pinned D2H of `nbytes` each (cudaMemcpyAsync
+    through torch): the floor of an e2e step that moves M in and out over PCIe."""
+    import torch
+    n = nbytes // np.dtype(dtype).itemsize
+    h_in = torch.empty(n, dtype=torch.float32 if dtype == np.float32 else torch.float64, pin_memory=True)
+    h_out = torch.empty_like(h_in).pin_memory()
+    d = torch.empty_like(h_in, device="cuda")
+    for _ in range(2):
+        d.copy_(h_in, non_blocking=True)
+        h_out.copy_(d, non_blocking=True)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    a.record()
+    for _ in range(reps):
+        d.copy_(h_in, non_blocking=True)
+        h_out.copy_(d, non_blocking=True)
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / reps
 
 
 def profile_summary(workload):
@@ -197,9 +236,12 @@ def profile_summary(workload):
         return {}
 
 
-def cpu_reference_time(wl, steps_max, budget_s, warmup=1):
-    """Reference Simulation<T>::step() (oracle/_ref) on the host cores, timed like
-    proj/src/benchmark.cpp:40-46 (steady clock, warm-up then measured steps)."""
+def cpu_reference_time(wl, warmup=1, measure=3, serial_measure=2):
+    """The reference's Simulation<T>::step() (oracle/_ref) on the host cores, timed as
+    proj/src/benchmark.cpp:40-46 does (make_simulation per backend, warm-up steps, then
+    steady-clock time of the measured steps; setup excluded), on a bounded sample: `measure`
+    steps on the parallel backend with every host thread and `serial_measure` steps on the
+    serial backend (1 core). FFTs are single-threaded in both, as in the reference."""
     # every host thread (torchrun exports OMP_NUM_THREADS=1 per rank; only rank 0 runs this, and
     # libgomp reads the variable when the reference library loads it below)
     cores = int(os.environ.get("MMB_REF_THREADS", len(os.sched_getaffinity(0))))
@@ -209,27 +251,33 @@ def cpu_reference_time(wl, steps_max, budget_s, warmup=1):
     if not ref.available():
         raise RuntimeError("oracle/_ref/libmmsim_ref.so missing (build with make -C oracle)")
     P = ref.Problem(nx, ny, nz, delta, a_ex, ms, hk, alpha, dt)
-    t0 = time.perf_counter()
-    sim = ref.RefSimulation(P, prec, backend="parallel")
-    setup = time.perf_counter() - t0
-    sim.set_m(random_state(nx, ny, nz, ms, np.float64 if prec == "f64" else np.float32))
-    for _ in range(warmup):
-        sim.step(1)
-    done, t = 0, 0.0
-    while done < max(1, steps_max):
-        t1 = time.perf_counter()
-        sim.step(1)
-        t += time.perf_counter() - t1
-        done += 1
-        if t > budget_s:
-            break
+    m0 = ref.random_unit_field(nx, ny, nz, ms, 20240 + nx, np.float64 if prec == "f64" else np.float32)
     n = nx * ny * nz
-    return {"value": n * done / t, "unit": UNIT, "cores": int(os.environ["OMP_NUM_THREADS"]),
-            "kind": "reference",
-            "sample": f"{done} full {nx}x{ny}x{nz} {prec} steps after {warmup} warm-up "
-                      f"(reference serial FFT + OpenMP field loops, FFTW-API shim; setup {setup:.1f}s "
-                      "excluded)",
-            "ms_per_step": 1e3 * t / done, "steps": done}
+    rows = []
+    for backend, steps, ncores in (("parallel", measure, cores), ("serial", serial_measure, 1)):
+        if steps <= 0:
+            continue
+        t0 = time.perf_counter()
+        sim = ref.RefSimulation(P, prec, backend=backend)
+        setup = time.perf_counter() - t0
+        sim.set_m(m0)
+        for _ in range(warmup):
+            sim.step(1)
+        t1 = time.perf_counter()
+        for _ in range(steps):
+            sim.step(1)
+        t = time.perf_counter() - t1
+        rows.append({"backend": backend, "cores": ncores, "warmup": warmup, "steps": steps,
+                     "ms_per_step": 1e3 * t / steps, "value": n * steps / t, "setup_s": round(setup, 2)})
+        del sim
+    par = rows[0]
+    return {"value": par["value"], "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"reference Simulation<{'float' if prec == 'f32' else 'double'}>::step() on {nx}x{ny}x{nz}, "
+                      f"timed as benchmark.cpp:40-46: {warmup} warm-up + {par['steps']} measured steps on the "
+                      f"parallel backend ({cores} threads; FFTs single-threaded, FFTW-API shim), setup excluded"
+                      + (f"; serial row: {warmup} + {rows[1]['steps']} steps on 1 core" if len(rows) > 1 else ""),
+            "ms_per_step": par["ms_per_step"], "steps": par["steps"], "rows": rows,
+            "cpu_model": cpu_model(), "nproc": os.cpu_count()}
 
 
 def run_reference(args, world, rank):
@@ -237,10 +285,16 @@ def run_reference(args, world, rank):
         return 0
     wl = args.workload
     nx, ny, nz, *_ , prec = WORKLOADS[wl]
-    c = cpu_reference_time(wl, args.steps, budget_s=float(os.environ.get("MMB_REF_BUDGET_S", "120")),
-                           warmup=min(args.warmup, 1))
+    if wl in SHARDED:
+        line = {"metric": METRIC, "impl": "reference", "unavailable":
+                f"the reference layout needs ~181 GB of host memory at {wl} (SURVEY.md §8(d)); no CPU run"}
+        print(json.dumps(line), flush=True)
+        return 0
+    # the reference arm times a bounded sample: per step ~2 s (parallel) / ~4 s (serial) at 512x512x8
+    measure = max(1, min(args.steps, int(os.environ.get("MMB_REF_STEPS", "10"))))
+    c = cpu_reference_time(wl, warmup=1, measure=measure, serial_measure=min(3, measure))
     line = {"metric": METRIC, "value": c["value"], "unit": UNIT, "n_gpus": world, "steps": c["steps"],
-            "warmup": min(args.warmup, 1), "ms_per_step": c["ms_per_step"], "higher_is_better": True,
+            "warmup": 1, "ms_per_step": c["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
             "impl": "reference",
             "config": {"workload": wl, "nx": nx, "ny": ny, "nz": nz, "parallelism": "host cores"},
@@ -270,11 +324,7 @@ def run_b200_sharded(args, world, rank, local):
     spec = ProblemSpec(name=wl, grid=Grid(nx, ny, nz, delta), material=MaterialParams(a_ex, ms, hk, alpha), dt=dt)
     sim = make_sharded_simulation(spec, Precision.f32 if prec == "f32" else Precision.f64, rank, world,
                                   bytes(nid.cpu().numpy()), device=local)
-    rng = np.random.default_rng(20240 + rank)
-    v = rng.uniform(-1.0, 1.0, (3, sim.nz_local, ny, nx)).astype(np.float32)
-    v /= np.maximum(np.sqrt((v * v).sum(0)), 0.1)
-    sim.set_magnetization((ms * v).astype(np.float32 if prec == "f32" else np.float64))
-    del v
+    sim.set_magnetization(random_state(nx, ny, nz, ms, prec, z0=sim.z0, nz_local=sim.nz_local))
     sim.time_steps(max(3, args.warmup))
     barrier(world)
     with ClockSampler(local) as clk:
@@ -335,7 +385,7 @@ def run_b200(args, world, rank, local):
     spec = ProblemSpec(name=wl, grid=Grid(nx, ny, nz, delta), material=MaterialParams(a_ex, ms, hk, alpha),
                        dt=dt)
     sim = make_simulation(spec, precision=Precision.f32 if prec == "f32" else Precision.f64, device=local)
-    m0 = random_state(nx, ny, nz, ms, dtype)
+    m0 = random_state(nx, ny, nz, ms, prec)
     sim.set_magnetization(m0)
 
     # ---- device-resident throughput (value)
@@ -347,8 +397,8 @@ def run_b200(args, world, rank, local):
     value = n * args.steps * world / (t_ms * 1e-3)
     ms_step = t_ms / args.steps
 
-    # ---- per-kernel times (eager launches with events) for the roofline
-    prof = sim.profile_step(max(5, min(args.steps, 20)))
+    # ---- per-kernel times (events between the kernels of replayed graphs) for the roofline
+    prof = sim.profile_step(max(16, min(args.steps, 64)))
     b_alg, kbytes = algorithmic_bytes(nx, ny, nz, w)
     peak, peak_kind = load_peaks()
     top = max(prof, key=prof.get)
@@ -379,14 +429,19 @@ def run_b200(args, world, rank, local):
         sim.step(1)
         sim.get_m_into(pin_out)
     te = max_over_ranks(world, time.perf_counter() - t0)
+    copy_ms = pcie_copy_ms(3 * n * w, dtype)
     e2e = {"value": n * args.steps * world / te, "unit": UNIT,
            "h2d_bytes_per_step": 3 * n * w, "d2h_bytes_per_step": 3 * n * w,
-           "api": "mmb_set_m + mmb_step(1) + mmb_get_m per step (libmmb.so C-ABI via ctypes)"}
+           "api": "mmb_set_m + mmb_step(1) + mmb_get_m per step (libmmb.so C-ABI via ctypes)",
+           "ms_per_step": 1e3 * te / args.steps,
+           "pcie_floor_ms": copy_ms + ms_step,
+           "note": "per step: pinned H2D of M, one graph-replayed step, pinned D2H of M (dependent, so the "
+                   "copies cannot overlap); pcie_floor_ms = device time of the same two copies + the step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_reference_time(wl, 2, budget_s=20.0, warmup=1)
+            cpu = cpu_reference_time(wl, warmup=1, measure=3, serial_measure=2)
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -417,11 +472,14 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="512x512x8_f32", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: 512x512x8_f32 on one GPU, 2048x2048x64_f32 z-slabs on N > 1")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     world, rank, local = dist_setup() if args.impl == "b200" else (
         int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    if args.workload is None:
+        args.workload = "512x512x8_f32" if world == 1 else "2048x2048x64_f32"
     if args.impl == "reference":
         return run_reference(args, world, rank)
     return run_b200(args, world, rank, local)

@@ -137,6 +137,17 @@ int mmb_profile_step(mmb_ctx* ctx, long long n, float* kernel_ms, int max_kernel
 int mmb_launches_per_step(mmb_ctx* ctx, int* out);
 /* Bytes of device memory held by the handle. */
 int mmb_device_bytes(mmb_ctx* ctx, size_t* out);
+/* The reference's seeded random initial state (random_unit_field, proj/src/validate.cpp:21-39:
+ * std::mt19937(seed), std::uniform_real_distribution<double>(-1, 1), draws of norm < 0.1
+ * rejected, ms * v / norm computed in double and cast to the precision): cells
+ * [first, first + count) of that sequence into SoA host arrays. Host-side utility (no device),
+ * used for the synthetic inputs of SURVEY.md §8(d). */
+int mmb_random_unit_field(unsigned seed, double ms, long long first, long long count, int precision,
+                          void* x, void* y, void* z);
+/* The demag path and kernel variants (template parameters, tiles, grids) this handle runs,
+ * as one NUL-terminated line (truncated to len - 1 bytes). Diagnostic; no reference
+ * counterpart. */
+int mmb_path_info(mmb_ctx* ctx, char* buf, size_t len);
 
 /* ---- multi-GPU: z-slab decomposition ------------------------------------
  * One process per GPU. Rank 0 creates an NCCL id with mmb_nccl_unique_id and shares it (e.g.

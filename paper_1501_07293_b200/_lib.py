@@ -18,7 +18,8 @@ EXPORTS = [
     "mmb_last_torque_sq", "mmb_run", "mmb_synchronize", "mmb_effective_field", "mmb_demag_field",
     "mmb_tensor_octant", "mmb_upload_tensor_octant", "mmb_time_steps", "mmb_profile_step",
     "mmb_launches_per_step", "mmb_device_bytes", "mmb_nccl_unique_id", "mmb_create_sharded",
-    "mmb_create_emulated", "mmb_slab", "mmb_validate", "mmb_string_free",
+    "mmb_create_emulated", "mmb_slab", "mmb_validate", "mmb_string_free", "mmb_path_info",
+    "mmb_random_unit_field",
 ]
 
 
@@ -95,6 +96,8 @@ def load():
     L.mmb_profile_step.argtypes = [vp, ll, C.POINTER(C.c_float), i, C.POINTER(i), C.c_char_p, sz]
     L.mmb_launches_per_step.argtypes = [vp, C.POINTER(i)]
     L.mmb_device_bytes.argtypes = [vp, C.POINTER(sz)]
+    L.mmb_path_info.argtypes = [vp, C.c_char_p, sz]
+    L.mmb_random_unit_field.argtypes = [C.c_uint, d, ll, ll, i, vp, vp, vp]
     L.mmb_nccl_unique_id.argtypes = [C.c_char_p]
     L.mmb_create_sharded.argtypes = [C.POINTER(MmbDesc), C.POINTER(MmbStage), i, i, i, C.c_char_p,
                                      C.POINTER(vp)]

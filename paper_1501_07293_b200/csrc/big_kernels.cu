@@ -9,6 +9,7 @@
 //
 // then the fused KXS (fast_kernels.cu) as on the small-nz path. All row transforms are the
 // register four-step of fft4.cuh with unit-stride global loads/stores.
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 
@@ -372,7 +373,29 @@ void launch_big_z(cx<T>* S2, const Geom& g, const cx<T>* tw, const T* kt, cudaSt
     check_launch();
 }
 
+template <typename T>
+std::string big_describe(const Geom& g) {
+    char buf[160];
+    const long long nrows = static_cast<long long>(g.xh) * 3 * g.nz;
+    int p = 0, la = 0;
+    switch (g.log2ly) {
+#define X(l) case l: p = YR<l>::P; la = YR<l>::LA; break;
+        MMB_Y_CASES(X)
+#undef X
+    }
+    int w = 0;
+    switch (g.log2lz) {
+#define X(l) case l: w = zw<T, l>(); break;
+        MMB_Z_CASES(X)
+#undef X
+    }
+    std::snprintf(buf, sizeof buf, "k_yrow<L%d> %s rows/cta=%d ctas=%lld; k_zmac<Lz%d> pencils/cta=%d", g.log2ly,
+                  la == 2 ? "pair" : "plain", p, (nrows + p - 1) / (p ? p : 1), g.log2lz, w);
+    return buf;
+}
+
 #define MMB_BINST(T)                                                                              \
+    template std::string big_describe<T>(const Geom&);                                           \
     template bool big_supported<T>(const Geom&);                                                 \
     template void prepare_big_kernels<T>(const Geom&);                                           \
     template void launch_big_yf<T>(const cx<T>*, cx<T>*, const Geom&, const cx<T>*, StepCtl*,     \

@@ -6,6 +6,8 @@
 
 #include <cuda_runtime.h>
 
+#include <string>
+
 #include "types.cuh"
 
 namespace mmb {
@@ -31,6 +33,9 @@ struct RowMap {
 };
 
 template <typename T> bool fast_supported(const Geom& g);
+// the kernel variants (template parameters, tiles, grids) the geometry selects
+template <typename T> std::string fast_describe(const Geom& g);
+template <typename T> std::string big_describe(const Geom& g);
 template <typename T> int fast_yz_kxb(const Geom& g, int* smem_bytes);
 template <typename T> void prepare_fast_kernels(const Geom& g);
 template <typename T>

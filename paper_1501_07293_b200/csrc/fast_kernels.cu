@@ -12,6 +12,7 @@
 //
 // Replaces proj/src/demag.cpp:67-145 (pad, 3 forward FFTs, MAC, 3 inverse FFTs, window
 // extract). 1/(Lx Ly Lz) is folded into the tensor spectrum (tensor_kernels.cu).
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -947,7 +948,38 @@ void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>
     check_launch();
 }
 
+// Kernel variants the geometry selects (tests assert that each production variant is covered).
+template <typename T>
+std::string fast_describe(const Geom& g) {
+    char buf[256];
+    int sb = 0;
+    const int kxb = fast_yz_kxb<T>(g, &sb);
+    std::string yz;
+    switch (g.log2ly) {
+#define X(l) case l: std::snprintf(buf, sizeof buf, "k_yz<L%d,ZM%d> kxb=%d nt=%d ctas=%d", l, g.nz == 1 ? 0 : 1, kxb, \
+                                   yz_threads<T, l>(), (g.xh + kxb - 1) / kxb); yz = buf; break;
+        MMB_FAST_CASES(X)
+#undef X
+        default: yz = "k_yz<?>";
+    }
+    std::string xs;
+    switch (g.log2lx) {
+#define X(l) case l: { const bool sm = xstep_small<l>(g); \
+        using XA = XS<l, 16, sizeof(T)>; using XB = XS<l, xs_pb(l), sizeof(T)>; \
+        const dim3 gr = sm ? xs_grid<XA>(g) : xs_grid<XB>(g); \
+        std::snprintf(buf, sizeof buf, "k_xstep<L%d,PB%d> tr=%d nt=%d %s grid=%ux%u", l, sm ? 16 : xs_pb(l), \
+                      sm ? XA::TR : XB::TR, sm ? XA::NT : XB::NT, \
+                      (sm ? XA::PAIR : XB::PAIR) ? "pair" : ((sm ? XA::WIDE : XB::WIDE) ? "wide" : "plain"), gr.x, gr.y); \
+        xs = buf; break; }
+        MMB_FAST_CASES(X)
+#undef X
+        default: xs = "k_xstep<?>";
+    }
+    return yz + "; " + xs;
+}
+
 #define MMB_FINST(T)                                                                            \
+    template std::string fast_describe<T>(const Geom&);                                        \
     template int fast_yz_kxb<T>(const Geom&, int*);                                            \
     template bool fast_supported<T>(const Geom&);                                              \
     template void prepare_fast_kernels<T>(const Geom&);                                        \

@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -124,6 +125,8 @@ public:
         yz_ = fast_supported<T>(gy);
         if (!yz_ && !big_supported<T>(g_))
             throw std::invalid_argument("mmb: grid not supported by the sharded path");
+        // every rank owns at least one kx column (its y/z launch runs the step prologue)
+        if (g_.xh < world) throw std::invalid_argument("mmb: z-slab sharding needs Lx/2+1 >= world size");
         slabs_ = split_range(d.nz, world);
         cols_ = split_range(g_.xh, world);
         exch_coeff_ = 2.0 * d.a_ex / (kMu0 * d.ms * d.ms * d.delta * d.delta);
@@ -353,6 +356,19 @@ public:
 
     int launches_per_step() const override {
         return static_cast<int>(ranks_.size()) * (yz_ ? 2 : 4);
+    }
+
+    std::string path_info() const override {
+        char head[200];
+        const Rank<T>& R = *ranks_[0];
+        std::snprintf(head, sizeof head, "path=sharded-%s world=%d mode=%s%s n=%dx%dx%d L=%dx%dx%d prec=%s slab=%d+%d cols=%d+%d",
+                      yz_ ? "yz" : "big", world_, emulated_ ? "emulated" : "nccl", peer_ ? "+peer" : "", d_.nx, d_.ny,
+                      d_.nz, g_.lx, g_.ly, g_.lz, sizeof(T) == 8 ? "f64" : "f32", R.z0, R.nzl, R.k0, R.ncols);
+        std::string s = head;
+        s += "; " + (yz_ ? fast_describe<T>(R.gc) : big_describe<T>(R.gc));
+        const std::string x = fast_describe<T>(R.gs);
+        s += "; slab " + x.substr(x.find("k_xstep"));
+        return s;
     }
 
     size_t device_bytes() const override {
@@ -602,6 +618,7 @@ private:
         ck(cudaMemcpyAsync(R->ctl.p, &c, sizeof(c), cudaMemcpyHostToDevice, stream_), "ctl upload");
         R->tpart_count = fast_xstep_blocks<T>(R->gs);
         R->tpart.alloc(R->tpart_count);
+        ck(cudaMemsetAsync(R->tpart.p, 0, R->tpart.bytes(), stream_), "memset");
         R->partial.alloc(3 * 1024);
         R->red.alloc(8);
         // zero the halo planes once (never read at the global ends: Neumann mask)
@@ -747,21 +764,42 @@ private:
         nck(ncclGroupEnd(), "ncclGroupEnd");
     }
 
+    // The first zero-|M| cell over all ranks (keys are (step << 36) | global cell, so the
+    // minimum is the reference's smallest cell of the earliest failing step). With NCCL the
+    // keys are min-all-reduced first: every rank raises the same error at the same call, and
+    // none is left waiting in a collective its failed peer never joins.
     void check_numerical() {
+        unsigned long long key = ~0ull;
+        for (auto& rp : ranks_) {
+            unsigned long long k;
+            if (!emulated_) {
+                unsigned long long* red = reinterpret_cast<unsigned long long*>(rp->red.p + 7);
+                ck(cudaMemcpyAsync(red, &rp->ctl.p->bad_key, sizeof(k), cudaMemcpyDeviceToDevice, stream_), "ctl");
+                nck(ncclAllReduce(red, red, 1, ncclUint64, ncclMin, comm_, stream_), "ncclAllReduce (error word)");
+                ck(cudaMemcpyAsync(&k, red, sizeof(k), cudaMemcpyDeviceToHost, stream_), "ctl");
+            } else {
+                ck(cudaMemcpyAsync(&k, &rp->ctl.p->bad_key, sizeof(k), cudaMemcpyDeviceToHost, stream_), "ctl");
+            }
+            ck(cudaStreamSynchronize(stream_), "ctl sync");
+            key = std::min(key, k);
+        }
+        if (key == ~0ull) return;
+        const long long cell = static_cast<long long>(key & ((1ull << 36) - 1));
+        const long long st = static_cast<long long>(key >> 36);
+        // as Solver::check_numerical: the step index returns to the failing step
+        step_ = st;
         for (auto& rp : ranks_) {
             StepCtl c;
             ck(cudaMemcpyAsync(&c, rp->ctl.p, sizeof(c), cudaMemcpyDeviceToHost, stream_), "ctl");
             ck(cudaStreamSynchronize(stream_), "ctl sync");
-            if (c.bad_key != ~0ull) {
-                const long long cell = static_cast<long long>(c.bad_key & ((1ull << 36) - 1));
-                const long long st = static_cast<long long>(c.bad_key >> 36);
-                const unsigned long long none = ~0ull;
-                ck(cudaMemcpyAsync(&rp->ctl.p->bad_key, &none, sizeof(none), cudaMemcpyHostToDevice, stream_), "reset");
-                ck(cudaStreamSynchronize(stream_), "reset sync");
-                throw numerical_error("renormalize: zero-magnitude magnetization at cell " + std::to_string(cell) +
-                                      " at step " + std::to_string(st));
-            }
+            c.bad_key = ~0ull;
+            c.step = c.cur_step = st;
+            ck(cudaMemcpyAsync(rp->ctl.p, &c, sizeof(c), cudaMemcpyHostToDevice, stream_), "reset");
+            ck(cudaStreamSynchronize(stream_), "reset sync");
         }
+        s_valid_ = false;
+        throw numerical_error("renormalize: zero-magnitude magnetization at cell " + std::to_string(cell) +
+                              " at step " + std::to_string(st));
     }
 
     void sync_and_check() {

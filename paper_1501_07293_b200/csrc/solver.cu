@@ -14,6 +14,7 @@
 #include <cstring>
 #include <memory>
 #include <new>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -25,6 +26,15 @@
 #include "validate.hpp"
 
 namespace mmb {
+
+// Event record that also works inside stream capture (an external event-record node), so the
+// per-kernel profile can be taken from inside a replayed graph.
+inline void record_event(cudaEvent_t ev, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    ck(cudaStreamIsCapturing(s, &cs), "cudaStreamIsCapturing");
+    if (cs == cudaStreamCaptureStatusActive) ck(cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal), "record");
+    else ck(cudaEventRecord(ev, s), "record");
+}
 
 template <typename T>
 class Solver final : public SolverBase {
@@ -106,6 +116,9 @@ public:
         partial_.alloc(3 * 1024);
         tpart_count_ = fast_ ? fast_xstep_blocks<T>(g) : llg_blocks(g);
         tpart_.alloc(std::max(llg_blocks(g), tpart_count_));
+        // last_torque_sq() before the first step reduces zeros (the reference's
+        // last_torque_sq_ starts at 0.0, llg.hpp)
+        ck(cudaMemsetAsync(tpart_.p, 0, tpart_.bytes(), stream_), "memset");
         red_.alloc(8);
         ctl_.alloc(1);
         ck(cudaMallocHost(&ctl_host_, sizeof(StepCtl)), "cudaMallocHost");
@@ -161,10 +174,9 @@ public:
     }
 
     ~Solver() override {
-        for (auto& ge : graph_)
-            if (ge) cudaGraphExecDestroy(ge);
-        for (auto& ge : batch_)
-            if (ge) cudaGraphExecDestroy(ge);
+        for (auto& row : graphs_)
+            for (auto& ge : row)
+                if (ge) cudaGraphExecDestroy(ge);
         if (ctl_host_) cudaFreeHost(ctl_host_);
         if (rec_host_) cudaFreeHost(rec_host_);
         if (stream_) cudaStreamDestroy(stream_);
@@ -179,6 +191,7 @@ public:
             ck(cudaMemcpyAsync(m_[cur_].p + c * n, src[c], n * sizeof(T), cudaMemcpyHostToDevice, stream_),
                "set_m");
         s_valid_ = false;
+        // the host arrays are borrowed for the call only: one synchronisation before returning
         ck(cudaStreamSynchronize(stream_), "set_m sync");
     }
 
@@ -191,20 +204,32 @@ public:
         sync_and_check();
     }
 
+    // n steps as graph replays: n = 32 q + binary digits of the rest, one graph of 2^b
+    // consecutive steps per digit (at most q + 5 graph launches, so a short run replays at the
+    // long-run rate); only the 1-step graph flips the ping-pong buffer
     void step(long long n) override {
         if (n > 0) prime();
-        // long runs replay a graph of kBatch consecutive steps (fewer graph launches)
-        for (; n >= kBatch; n -= kBatch) {
-            ensure_batch_graph(cur_);
-            ck(cudaGraphLaunch(batch_[cur_], stream_), "cudaGraphLaunch");
-            step_ += kBatch;
-        }
-        for (long long i = 0; i < n; ++i) {
-            ensure_graph(cur_);
-            ck(cudaGraphLaunch(graph_[cur_], stream_), "cudaGraphLaunch");
-            cur_ ^= 1;
-            ++step_;
-        }
+        for (; n >= (1LL << kMaxLog2Batch); n -= (1LL << kMaxLog2Batch)) launch_graph(kMaxLog2Batch);
+        for (int b = kMaxLog2Batch - 1; b >= 0; --b)
+            if (n & (1LL << b)) launch_graph(b);
+    }
+
+    void launch_graph(int b) {
+        ensure_graph(b, cur_);
+        ck(cudaGraphLaunch(graphs_[b][cur_], stream_), "cudaGraphLaunch");
+        if (b == 0) cur_ ^= 1;
+        step_ += 1LL << b;
+    }
+
+    // instantiate every graph step(n) will replay (outside any timed region)
+    void prepare_graphs(long long n) {
+        int cur = cur_;
+        if (n >= (1LL << kMaxLog2Batch)) ensure_graph(kMaxLog2Batch, cur);
+        for (int b = kMaxLog2Batch - 1; b >= 0; --b)
+            if (n & (1LL << b)) {
+                ensure_graph(b, cur);
+                if (b == 0) cur ^= 1;
+            }
     }
 
     long long step_index() const override { return step_; }
@@ -355,12 +380,8 @@ public:
     }
 
     float time_steps(long long n) override {
-        ensure_graph(0);
-        ensure_graph(1);
-        if (n >= kBatch) {
-            ensure_batch_graph(0);
-            ensure_batch_graph(1);
-        }
+        prime();
+        prepare_graphs(n);
         cudaEvent_t a, b;
         ck(cudaEventCreate(&a), "event");
         ck(cudaEventCreate(&b), "event");
@@ -376,30 +397,49 @@ public:
         return ms;
     }
 
+    // Per-kernel device time from inside replayed graphs: a graph of kProfSteps consecutive
+    // steps with an external event-record node between consecutive kernels (the same kernels
+    // and launch parameters as the production graphs, minus any programmatic-launch overlap
+    // across the event nodes), replayed until n steps ran; mean per step per kernel.
     int profile_step(long long n, float* out, int maxk, std::string& names) override {
-        // Eager launches with an event between kernels; per-kernel mean over n steps.
+        constexpr int kProfSteps = 16; // even: the graph returns M to the same buffer
         const std::vector<std::string> kn = kernel_names();
         const int nk = static_cast<int>(kn.size());
-        std::vector<cudaEvent_t> ev(nk + 1);
+        std::vector<cudaEvent_t> ev(static_cast<size_t>(kProfSteps) * (nk + 1));
         for (auto& e : ev) ck(cudaEventCreate(&e), "event");
-        std::vector<double> acc(nk, 0.0);
         prime();
-        for (long long s = 0; s < n; ++s) {
-            ck(cudaEventRecord(ev[0], stream_), "record");
-            enqueue_step_eager(cur_, ev.data());
-            ck(cudaEventSynchronize(ev[nk]), "sync");
-            for (int k = 0; k < nk; ++k) {
-                float ms = 0.f;
-                cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
-                acc[k] += ms;
-            }
-            cur_ ^= 1;
-            ++step_;
+        cudaGraph_t gr;
+        cudaGraphExec_t ge = nullptr;
+        ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+        for (int i = 0; i < kProfSteps; ++i) {
+            cudaEvent_t* e = ev.data() + static_cast<size_t>(i) * (nk + 1);
+            record_event(e[0], stream_);
+            enqueue_step_eager(cur_ ^ (i & 1), e);
         }
+        ck(cudaStreamEndCapture(stream_, &gr), "end capture");
+        ck(cudaGraphInstantiate(&ge, gr, 0), "graph instantiate");
+        cudaGraphDestroy(gr);
+        std::vector<double> acc(nk, 0.0);
+        long long done = 0;
+        const long long reps = std::max<long long>(1, (n + kProfSteps - 1) / kProfSteps);
+        for (long long r = 0; r < reps; ++r) {
+            ck(cudaGraphLaunch(ge, stream_), "cudaGraphLaunch");
+            ck(cudaStreamSynchronize(stream_), "sync");
+            for (int i = 0; i < kProfSteps; ++i)
+                for (int k = 0; k < nk; ++k) {
+                    float ms = 0.f;
+                    const size_t b = static_cast<size_t>(i) * (nk + 1);
+                    ck(cudaEventElapsedTime(&ms, ev[b + k], ev[b + k + 1]), "elapsed");
+                    acc[k] += ms;
+                }
+            done += kProfSteps;
+            step_ += kProfSteps;
+        }
+        cudaGraphExecDestroy(ge);
         for (auto& e : ev) cudaEventDestroy(e);
         names.clear();
         for (int k = 0; k < nk; ++k) {
-            if (k < maxk) out[k] = static_cast<float>(acc[k] / std::max<long long>(1, n));
+            if (k < maxk) out[k] = static_cast<float>(acc[k] / static_cast<double>(done));
             names += kn[k];
             if (k + 1 < nk) names += ";";
         }
@@ -412,6 +452,22 @@ public:
     void slab(int& z0, int& nzl) const override {
         z0 = 0;
         nzl = g_.nz;
+    }
+
+    std::string path_info() const override {
+        char head[160];
+        std::snprintf(head, sizeof head, "path=%s n=%dx%dx%d L=%dx%dx%d prec=%s pdl=%d", yz_ ? "yz" : (fast_ ? "big" : "general"),
+                      g_.nx, g_.ny, g_.nz, g_.lx, g_.ly, g_.lz, sizeof(T) == 8 ? "f64" : "f32", pdl_ ? 1 : 0);
+        std::string s = head;
+        if (fast_ && yz_) s += "; " + fast_describe<T>(g_);
+        else if (fast_) s += "; " + big_describe<T>(g_) + "; " + fast_describe_xstep(g_);
+        return s;
+    }
+
+    static std::string fast_describe_xstep(const Geom& g) {
+        const std::string d = fast_describe<T>(g);
+        const size_t k = d.find("k_xstep");
+        return k == std::string::npos ? d : d.substr(k);
     }
 
     size_t device_bytes() const override {
@@ -486,7 +542,7 @@ private:
     void enqueue_demag(const T* m, T* h, int prologue, cudaEvent_t* ev = nullptr) {
         int k = 1;
         auto mark = [&]() {
-            if (ev) ck(cudaEventRecord(ev[k++], stream_), "record");
+            if (ev) record_event(ev[k++], stream_);
         };
         if (fast_) {
             // S is reused as scratch: it no longer holds the x spectrum of the current M
@@ -527,7 +583,7 @@ private:
     // the profiling events.
     void enqueue_yz(int prologue, int* k, cudaEvent_t* ev) {
         auto mark = [&]() {
-            if (ev && k) ck(cudaEventRecord(ev[(*k)++], stream_), "record");
+            if (ev && k) record_event(ev[(*k)++], stream_);
         };
         if (yz_) {
             launch_fast_yz<T>(S_.p, g_, twy_.p, kspec_.p, ctl_.p, st_, prologue, stream_, pdl_);
@@ -548,12 +604,12 @@ private:
             enqueue_yz(1, &k, ev);
             launch_fast_xstep<T>(S_.p, m_[cur].p, m_[cur ^ 1].p, g_, twx_.p, exch_coeff_, aniso_coeff_,
                                  ctl_.p, tpart_.p, stream_, pdl_);
-            if (ev) ck(cudaEventRecord(ev[k], stream_), "record");
+            if (ev) record_event(ev[k], stream_);
             return;
         }
         enqueue_demag(m_[cur].p, hd_.p, 1, ev);
         launch_llg<T>(0, m_[cur].p, hd_.p, m_[cur ^ 1].p, g_, exch_coeff_, aniso_coeff_, ctl_.p, tpart_.p, stream_);
-        if (ev) ck(cudaEventRecord(ev[kernel_names().size()], stream_), "record");
+        if (ev) record_event(ev[kernel_names().size()], stream_);
     }
 
     void enqueue_heff() {
@@ -561,23 +617,14 @@ private:
         launch_llg<T>(1, m_[cur_].p, hd_.p, heff_.p, g_, exch_coeff_, aniso_coeff_, ctl_.p, tpart_.p, stream_);
     }
 
-    void ensure_batch_graph(int cur) {
-        if (batch_[cur]) return;
+    // graph of 2^b consecutive steps starting from buffer `cur`
+    void ensure_graph(int b, int cur) {
+        if (graphs_[b][cur]) return;
         cudaGraph_t gr;
         ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
-        for (int i = 0; i < kBatch; ++i) enqueue_step_eager(cur ^ (i & 1));
+        for (int i = 0; i < (1 << b); ++i) enqueue_step_eager(cur ^ (i & 1));
         ck(cudaStreamEndCapture(stream_, &gr), "end capture");
-        ck(cudaGraphInstantiate(&batch_[cur], gr, 0), "graph instantiate");
-        cudaGraphDestroy(gr);
-    }
-
-    void ensure_graph(int cur) {
-        if (graph_[cur]) return;
-        cudaGraph_t gr;
-        ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
-        enqueue_step_eager(cur);
-        ck(cudaStreamEndCapture(stream_, &gr), "end capture");
-        ck(cudaGraphInstantiate(&graph_[cur], gr, 0), "graph instantiate");
+        ck(cudaGraphInstantiate(&graphs_[b][cur], gr, 0), "graph instantiate");
         cudaGraphDestroy(gr);
     }
 
@@ -600,10 +647,18 @@ private:
         if (key != ~0ull) {
             const long long cell = static_cast<long long>(key & ((1ull << 36) - 1));
             const long long st = static_cast<long long>(key >> 36);
-            // reset so the handle can report later failures
-            const unsigned long long none = ~0ull;
-            ck(cudaMemcpyAsync(&ctl_.p->bad_key, &none, sizeof(none), cudaMemcpyHostToDevice, stream_), "reset");
+            // The reference's step() throws before ++step_ (llg.cpp:102-107): the step index
+            // returns to the failing step (steps queued after it ran on a degenerate state; M
+            // is unspecified after a numerical failure, as in the reference). Reset the error
+            // word so the handle can report later failures.
+            step_ = st;
+            StepCtl* c = ctl_host_;
+            c->bad_key = ~0ull;
+            c->step = st;
+            c->cur_step = st;
+            ck(cudaMemcpyAsync(ctl_.p, c, sizeof(StepCtl), cudaMemcpyHostToDevice, stream_), "reset");
             ck(cudaStreamSynchronize(stream_), "reset sync");
+            s_valid_ = false;
             throw numerical_error("renormalize: zero-magnitude magnetization at cell " +
                                   std::to_string(cell) + " at step " + std::to_string(st));
         }
@@ -625,11 +680,10 @@ private:
     double* rec_host_ = nullptr;
     DevBuf<StepCtl> ctl_;
     StepCtl* ctl_host_ = nullptr;
-    cudaGraphExec_t graph_[2] = {nullptr, nullptr};
-    static constexpr int kBatch = 32; // even: a batch returns M to the same buffer
+    static constexpr int kMaxLog2Batch = 5; // graphs of 1, 2, 4, 8, 16 and 32 steps
+    cudaGraphExec_t graphs_[kMaxLog2Batch + 1][2] = {};
     // programmatic dependent launch between the per-step kernels: pays on large grids only
     bool pdl_ = false;
-    cudaGraphExec_t batch_[2] = {nullptr, nullptr};
     int cur_ = 0;
     bool fast_ = false;
     bool yz_ = false;       // fast path with the fused shared-memory y/z kernel
@@ -884,6 +938,51 @@ int mmb_slab(mmb_ctx* ctx, int* z0, int* nz_local) {
     if (!ctx || !z0 || !nz_local) return bad("mmb_slab");
     ctx->s->slab(*z0, *nz_local);
     return MMB_OK;
+}
+
+int mmb_random_unit_field(unsigned seed, double ms, long long first, long long count, int precision,
+                          void* x, void* y, void* z) {
+    if (!x || !y || !z || first < 0 || count < 0 || (precision != MMB_F32 && precision != MMB_F64))
+        return bad("mmb_random_unit_field");
+    return guarded([&] {
+        // proj/src/validate.cpp:21-39: mt19937(seed), U(-1, 1) from libstdc++, rejection of
+        // norm < 0.1, ms * v / norm in double, then cast to T. Cells before `first` are drawn
+        // and dropped (a slab of the same global field).
+        std::mt19937 rng(seed);
+        std::uniform_real_distribution<double> dist(-1.0, 1.0);
+        for (long long i = 0; i < first + count; ++i) {
+            double a, b, c, norm;
+            do {
+                a = dist(rng);
+                b = dist(rng);
+                c = dist(rng);
+                norm = std::sqrt(a * a + b * b + c * c);
+            } while (norm < 0.1);
+            if (i < first) continue;
+            const long long k = i - first;
+            if (precision == MMB_F64) {
+                static_cast<double*>(x)[k] = ms * a / norm;
+                static_cast<double*>(y)[k] = ms * b / norm;
+                static_cast<double*>(z)[k] = ms * c / norm;
+            } else {
+                static_cast<float*>(x)[k] = static_cast<float>(ms * a / norm);
+                static_cast<float*>(y)[k] = static_cast<float>(ms * b / norm);
+                static_cast<float*>(z)[k] = static_cast<float>(ms * c / norm);
+            }
+        }
+        return MMB_OK;
+    });
+}
+
+int mmb_path_info(mmb_ctx* ctx, char* buf, size_t len) {
+    if (!ctx || !buf || len == 0) return bad("mmb_path_info");
+    return guarded([&] {
+        const std::string s = ctx->s->path_info();
+        const size_t k = std::min(s.size(), len - 1);
+        std::memcpy(buf, s.data(), k);
+        buf[k] = 0;
+        return MMB_OK;
+    });
 }
 
 int mmb_device_bytes(mmb_ctx* ctx, size_t* out) {

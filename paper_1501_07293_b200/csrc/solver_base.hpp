@@ -77,6 +77,8 @@ public:
     // global z range whose M this handle's set_m/get_m exchange (the whole grid except for
     // one rank of a NCCL-sharded solver)
     virtual void slab(int& z0, int& nz_local) const = 0;
+    // demag path and kernel variants this handle runs (mmb_path_info)
+    virtual std::string path_info() const = 0;
 };
 
 

@@ -231,6 +231,27 @@ class Simulation:
         _lib.check(self._L.mmb_device_bytes(self._h, C.byref(v)))
         return v.value
 
+    def path_info(self) -> str:
+        """The demag path and kernel variants (templates, tiles, grids) this handle runs."""
+        buf = C.create_string_buffer(1024)
+        _lib.check(self._L.mmb_path_info(self._h, buf, 1024))
+        return buf.value.decode()
+
+
+def random_unit_field(nx: int, ny: int, nz: int, ms: float, seed: int, precision: Precision = Precision.f64,
+                      z0: int = 0, nz_local: Optional[int] = None) -> np.ndarray:
+    """The reference's seeded random start (random_unit_field, proj/src/validate.cpp:21-39),
+    generated by libmmb.so's host utility: [3, nz_local, ny, nx] for planes [z0, z0 + nz_local)
+    of the global nx x ny x nz field."""
+    nzl = nz - z0 if nz_local is None else nz_local
+    plane = nx * ny
+    dt = np.float64 if precision == Precision.f64 else np.float32
+    out = np.empty((3, nzl, ny, nx), dtype=dt)
+    _lib.check(_lib.load().mmb_random_unit_field(seed, ms, z0 * plane, nzl * plane,
+                                                  _lib.MMB_F64 if precision == Precision.f64 else _lib.MMB_F32,
+                                                  _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
+    return out
+
 
 def nccl_unique_id() -> bytes:
     """128-byte NCCL id (rank 0 creates it; broadcast it to the other ranks)."""

@@ -5,6 +5,8 @@ i.e. run in the build container, never on the GPU box).
     python tests/golden/make_golden.py fields            # small H_eff / step vectors (seconds)
     python tests/golden/make_golden.py traj sp4_128_f64  # full SP#4 trajectories (minutes)
     python tests/golden/make_golden.py fixture           # copy of the reference's own SP#4 TSV
+    python tests/golden/make_golden.py film film256_f32  # 256x256x1 film relaxation (~45 min)
+    python tests/golden/make_golden.py crit6             # acceptance criterion 6 energies (minutes)
 
 Trajectory runs replay the reference's Simulation<T>::run exactly (proj/src/llg.cpp:110-124)
 with cadence 1000 and record <m> with %.17g so the B200 run can be compared at 1e-6.
@@ -79,6 +81,54 @@ def make_fields():
     print("wrote fields_small.npz", len(out))
 
 
+# BASELINE configs[1]: 256x256x1 film, SURVEY.md §8(d) input (2): SP#3 overrides nx=ny=256, nz=1,
+# delta=3, a_ex=1.3e7, ms=800, hk=0, alpha=0.5, dt=5e-6, no field; random start from the
+# reference generator (proj/src/validate.cpp:21-39) with seed 20240 + nx; 20 000 steps at
+# cadence 100.
+FILM = {"film256_f32": "f32", "film256_f64": "f64"}
+FILM_STEPS, FILM_CADENCE = 20000, 100
+
+
+def film_problem():
+    return ref.Problem(256, 256, 1, 3.0, 1.3e7, 800.0, 0.0, 0.5, 5e-6, [])
+
+
+def make_film(name):
+    prec = FILM[name]
+    P = film_problem()
+    sim = ref.RefSimulation(P, prec, backend="parallel")
+    sim.set_m(ref.random_unit_field(256, 256, 1, 800.0, 20240 + 256, np.float64 if prec == "f64" else np.float32))
+    recs = []
+    t0 = time.time()
+    sim.run(FILM_STEPS, FILM_CADENCE, records=recs)
+    path = os.path.join(HERE, f"traj_{name}.tsv")
+    with open(path, "w") as f:
+        f.write(f"# reference Simulation<{'double' if prec == 'f64' else 'float'}>::run, film 256x256x1 delta=3 "
+                f"a_ex=1.3e7 ms=800 hk=0 alpha=0.5 dt=5e-6, random_unit_field seed 20496, cadence "
+                f"{FILM_CADENCE}, shim FFT; {time.time() - t0:.0f}s\n")
+        for s_, mx, my, mz in recs:
+            f.write(f"{s_}\t{mx:.17g}\t{my:.17g}\t{mz:.17g}\n")
+    print("wrote", path, len(recs), f"{time.time() - t0:.0f}s")
+
+
+def make_crit6():
+    """Acceptance criterion 6 (proj/tests/acceptance.cpp:307-336): SP#3 16^3 f64 from uniform
+    +x, energy after each of 200 bursts of 100 steps, final max torque."""
+    P = ref.Problem(16, 16, 16, 1.0, 1e7, 1000.0, 100.0, 0.5, 1e-5, [])
+    sim = ref.RefSimulation(P, "f64")
+    rows = [(0, sim.energy()) + sim.average_unit()]
+    for _ in range(200):
+        sim.run(100, 0)
+        rows.append((sim.step_index(), sim.energy()) + sim.average_unit())
+    path = os.path.join(HERE, "crit6_sp3_16_f64.tsv")
+    with open(path, "w") as f:
+        f.write(f"# reference Simulation<double> SP#3 16^3 (criterion 6): step, energy, <m>; final max_torque "
+                f"{sim.max_torque():.17g}\n")
+        for r in rows:
+            f.write("\t".join([str(r[0])] + [f"{v:.17g}" for v in r[1:]]) + "\n")
+    print("wrote", path, len(rows))
+
+
 def make_traj(name):
     nx, ny, nz, delta, prec = TRAJ[name]
     P, steps, cad = sp4_problem(nx, ny, nz, delta)
@@ -102,6 +152,11 @@ if __name__ == "__main__":
         make_fields()
     elif what == "fixture":
         make_fixture()
+    elif what == "film":
+        for n in sys.argv[2:] or list(FILM):
+            make_film(n)
+    elif what == "crit6":
+        make_crit6()
     elif what == "traj":
         for n in sys.argv[2:] or list(TRAJ):
             make_traj(n)

@@ -151,3 +151,16 @@ def test_mmsim_library_with_b200_backend_builds_and_exports_mmsim_h():
     r = subprocess.run([INTEG_CHECK, str(os.path.join(ROOT, "build"))], capture_output=True, text=True, timeout=120)
     assert r.returncode == 2 and "no CUDA device" in r.stdout, r.stdout + r.stderr
     assert "FAIL" not in r.stdout
+
+
+def test_random_unit_field_is_the_reference_generator(refsolver):
+    """mmb_random_unit_field (host utility) reproduces the reference's random_unit_field
+    (proj/src/validate.cpp:21-39, via oracle/_ref) bitwise, and a slab of it equals the same
+    planes of the whole field."""
+    import numpy as np
+    from paper_1501_07293_b200 import Precision, random_unit_field
+    for prec, dt in ((Precision.f64, np.float64), (Precision.f32, np.float32)):
+        want = refsolver.random_unit_field(29, 7, 6, 1000.0, 20240 + 29, dt)
+        assert np.array_equal(random_unit_field(29, 7, 6, 1000.0, 20240 + 29, prec), want)
+        assert np.array_equal(random_unit_field(29, 7, 6, 1000.0, 20240 + 29, prec, z0=3, nz_local=2),
+                              want[:, 3:5])

@@ -248,6 +248,15 @@ def test_degenerate_cell_is_numerical_error():
     sim.step(3)
     with pytest.raises(NumericalError, match=r"zero-magnitude magnetization at cell 1 at step 0"):
         sim.average_unit()
+    # the reference throws before ++step_ (proj/src/llg.cpp:102-107): the index stays at the
+    # failing step
+    assert sim.step_index() == 0
+
+
+def test_last_torque_sq_starts_at_zero():
+    # the reference's last_torque_sq_ starts at 0.0 (proj/include/mmsim/llg.hpp:114)
+    for grid in [(4, 4, 2, 1.0), (128, 32, 1, 3.90625), (40, 24, 9, 2.0)]:
+        assert b200(spec(*grid)).last_torque_sq() == 0.0
 
 
 def test_streamed_records_match_per_step_averages():
@@ -441,6 +450,16 @@ def test_sharded_pipeline_equals_single_device(grid, world, prec, peer, monkeypa
     assert np.array_equal(a, b), rel(a, b)
     assert np.allclose(shard.average_unit(), single.average_unit(), rtol=0, atol=1e-12)
     assert abs(shard.last_torque_sq() - single.last_torque_sq()) <= 1e-12 * single.last_torque_sq()
+
+
+def test_sharding_needs_a_kx_column_per_rank():
+    """Every rank owns at least one kx column (its y/z launch runs the step prologue): nx = 2
+    gives Lx/2+1 = 3 columns, so 4 ranks are rejected."""
+    from paper_1501_07293_b200 import Precision
+    from paper_1501_07293_b200.simulation import make_emulated_sharded_simulation
+    with pytest.raises(ValueError, match="Lx/2"):
+        make_emulated_sharded_simulation(spec(2, 4, 8, 1.0), Precision.f32, 4)
+    make_emulated_sharded_simulation(spec(2, 4, 8, 1.0), Precision.f32, 3)
 
 
 def test_nccl_sharded_single_rank_matches_single_device(monkeypatch):
