@@ -12,23 +12,29 @@
 
 namespace mmb {
 
-// Rows of the y/z stage read from and written back to the ranks' own slab spectra instead of a
-// transposed column buffer (peer-memory sharding, shard.cu): row (kx, c, z) of this rank's
-// column range lives in rank q = owner(z) at base[q][((k0 + kx) * 3 + c) * nzl_q + z - z0[q]]
-// rows of ny values. base[q] may be another GPU's memory (CUDA IPC, NVLink loads/stores).
+// Rows of the y/z stage gathered from per-rank spectrum blocks instead of one contiguous column
+// buffer (slab sharding, shard.cu): row (kx, c, z) of a launch (kx counted from the launch's
+// first column) lives in block q = owner(z) at
+//   base[q][((kb[q] + kx) * 3 + c) * nzl_q + z - z0[q]]   (rows of ny values).
+// A block is a rank's own slab spectrum S_loc[kx][c][z_loc][y] (kb = that rank's global first
+// column of the launch) or the receive buffer an all-to-all filled with one peer's planes of
+// this rank's columns (kb = the launch's first local column). `local`: every block is in this
+// GPU's memory (whole rows are then staged with TMA bulk copies); otherwise base[q] may be
+// another GPU's memory (CUDA IPC peer mapping, NVLink loads/stores) and rows are plain loads.
 // world == 0: rows are the contiguous local column buffer.
 constexpr int kMaxRanks = 8;
 template <typename T>
 struct RowMap {
     cx<T>* base[kMaxRanks];
+    int kb[kMaxRanks];
     int z0[kMaxRanks + 1]; // slab starts, z0[world] = nz
     int world = 0;
-    int k0 = 0;
+    int local = 0;
     __device__ __forceinline__ cx<T>* row(int kx, int c, int z, int ny) const {
         int q = 0;
         while (z >= z0[q + 1]) ++q;
         const long long nzl = z0[q + 1] - z0[q];
-        return base[q] + ((static_cast<long long>(k0 + kx) * 3 + c) * nzl + (z - z0[q])) * ny;
+        return base[q] + ((static_cast<long long>(kb[q] + kx) * 3 + c) * nzl + (z - z0[q])) * ny;
     }
 };
 

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(x_pairs<LOG2L>() * Split<LOG2L>::N2)
         constexpr int NO = N1 == 1 ? 1 : N1 / 2;
         DftP<N1, +1, N1, NO>::run(u);
         const int ya = y0 + 2 * pb, yb = ya + 1;
-        T* ha = h + ((static_cast<long long>(c) * nz + z) * ny + ya) * nx;
+        T* ha = h + c * g.cs + (static_cast<long long>(z) * ny + ya) * nx; // component stride cs (slabs: halo)
         T* hb = ha + nx;
 #pragma unroll
         for (int k1 = 0; k1 < NO; ++k1) {
@@ -269,12 +269,12 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
     // their shared-memory rows, in flight together while the twiddles are staged. Rows in
     // peer memory are read with plain loads.
     const unsigned rowbytes = static_cast<unsigned>(ny * sizeof(cx<T>));
-    const bool bulk = (rowbytes % 16) == 0 && !PEER;
+    const bool bulk = (rowbytes % 16) == 0 && (!PEER || rm.local);
     if (tid == 0) {
         mbar_init(&bar, 1);
         if (bulk) {
             mbar_expect_tx(&bar, rowbytes * rows);
-            for (int r = 0; r < rows; ++r) bulk_g2s(sm + r * RP, gblk + static_cast<long long>(r) * ny, rowbytes, &bar);
+            for (int r = 0; r < rows; ++r) bulk_g2s(sm + r * RP, grow(r), rowbytes, &bar);
         }
     }
     stage_twiddles<T, LOG2L>(tws, tw);
@@ -957,7 +957,7 @@ std::string fast_describe(const Geom& g) {
     std::string yz;
     switch (g.log2ly) {
 #define X(l) case l: std::snprintf(buf, sizeof buf, "k_yz<L%d,ZM%d> kxb=%d nt=%d ctas=%d", l, g.nz == 1 ? 0 : 1, kxb, \
-                                   yz_threads<T, l>(), (g.xh + kxb - 1) / kxb); yz = buf; break;
+                                   yz_threads<T, l>(), kxb > 0 ? (g.xh + kxb - 1) / kxb : 0); yz = buf; break;
         MMB_FAST_CASES(X)
 #undef X
         default: yz = "k_yz<?>";

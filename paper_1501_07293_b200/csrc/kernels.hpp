@@ -34,6 +34,8 @@ void prepare_fft_kernels(const Geom& g);
 // ---- local terms + LLG update (llg_kernels.cu, compiled without FMA contraction) -------
 // mode 0: H_eff = hd + exchange + anisotropy + applied; Euler; renormalise; write m_out.
 // mode 1: write H_eff only (m_out receives H_eff), no state change.
+// m, hd and out share the component stride g.cs; the exchange mask uses the global plane
+// g.z0 + k of g.nz_g (a slab's halo planes must then hold the neighbouring planes).
 template <typename T>
 void launch_llg(int mode, const T* m, const T* hd, T* out, const Geom& g, double exch_coeff,
                 double aniso_coeff, StepCtl* ctl, double* tpart, cudaStream_t stream);
@@ -45,12 +47,14 @@ void launch_torque_partials(const double* tpart, int nb, StepCtl* ctl, cudaStrea
 // partial[nblk*3] then out[3] (sum, not mean).
 template <typename T>
 void launch_sum3(const T* m, long long n, long long cs, double* partial, double* out, cudaStream_t stream);
-// max_cell |M x H|^2 in fp64 -> *out_bits (double bits, atomicMax).
+// max over the n cells of |M x H|^2 in fp64 -> *out_bits (double bits, atomicMax); component
+// stride cs of both fields.
 template <typename T>
-void launch_torque_max(const T* m, const T* h, long long n, unsigned long long* out_bits,
+void launch_torque_max(const T* m, const T* h, long long n, long long cs, unsigned long long* out_bits,
                        cudaStream_t stream);
 // Total energy (proj/src/energy.cpp:5-64) partial sums: local (anis+demag+zeeman) and
-// exchange bonds, fp64, deterministic -> out[2].
+// exchange bonds, fp64, deterministic -> out[2]. Over the g.n cells of g (component stride
+// g.cs; a slab's +z bonds of its last plane read the halo plane above).
 template <typename T>
 void launch_energy(const T* m, const T* hd, const Geom& g, double ku_over_ms2,
                    const StepCtl* ctl, double* partial, double* out, cudaStream_t stream);

@@ -76,14 +76,16 @@ template <typename T, int MODE>
 __global__ void __launch_bounds__(kLlgThreads) k_llg(const T* __restrict__ m, const T* __restrict__ hd,
                                                      T* __restrict__ out, Geom g, T coeff, T kan,
                                                      StepCtl* ctl, double* __restrict__ tpart) {
-    const int n = static_cast<int>(g.n);
-    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    // component stride cs (= n on one device; a slab's buffers carry halo planes) and the
+    // global plane index for the Neumann mask (slabs: the halo planes hold the neighbours')
+    const long long n = g.cs;
+    const int nx = g.nx, ny = g.ny, nzg = g.nz_g;
     const int sy = nx, sz = nx * ny;
     const int tx = threadIdx.x, ty = threadIdx.y, lt = ty * kTileX + tx;
     const long long cur_step = ctl->cur_step;
     if (MODE == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lt == 0)
         ctl->step = cur_step + 1;
-    const int i = blockIdx.x * kTileX + tx, j = blockIdx.y * kTileY + ty, k = blockIdx.z;
+    const int i = blockIdx.x * kTileX + tx, j = blockIdx.y * kTileY + ty, k = blockIdx.z, kg = g.z0 + k;
     double tmax = 0.0;
     if (i < nx && j < ny) {
         const T ax = static_cast<T>(ctl->field[0]);
@@ -95,9 +97,9 @@ __global__ void __launch_bounds__(kLlgThreads) k_llg(const T* __restrict__ m, co
         const T* pz = py + n;
         const T mx = __ldg(px), my = __ldg(py), mz = __ldg(pz);
         T hx = __ldg(hd + f), hy = __ldg(hd + n + f), hz = __ldg(hd + 2 * n + f);
-        hx += coeff * exch1(px, i, j, k, nx, ny, nz, sy, sz);
-        hy += coeff * exch1(py, i, j, k, nx, ny, nz, sy, sz);
-        hz += coeff * exch1(pz, i, j, k, nx, ny, nz, sy, sz);
+        hx += coeff * exch1(px, i, j, kg, nx, ny, nzg, sy, sz);
+        hy += coeff * exch1(py, i, j, kg, nx, ny, nzg, sy, sz);
+        hz += coeff * exch1(pz, i, j, kg, nx, ny, nzg, sy, sz);
         hx += kan * mx;
         hx += ax;
         hy += ay;
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(kLlgThreads) k_llg(const T* __restrict__ m, co
             const T mag = sqrt(nxv * nxv + nyv * nyv + nzv * nzv);
             if (mag == T(0)) {
                 atomicMin(&ctl->bad_key, (static_cast<unsigned long long>(cur_step) << 36) |
-                                             static_cast<unsigned long long>(f));
+                                             static_cast<unsigned long long>(f + static_cast<long long>(g.z0) * sz));
             } else {
                 const T scale = ms / mag;
                 nxv *= scale;
@@ -198,12 +200,12 @@ __global__ void k_final_sum(const double* __restrict__ partial, int nblk, double
 
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_torque_max(const T* __restrict__ m, const T* __restrict__ h,
-                                                            long long n, unsigned long long* out) {
+                                                            long long n, long long cs, unsigned long long* out) {
     double t = 0.0;
     for (long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; f < n;
          f += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const double mx = m[f], my = m[n + f], mz = m[2 * n + f];
-        const double hx = h[f], hy = h[n + f], hz = h[2 * n + f];
+        const double mx = m[f], my = m[cs + f], mz = m[2 * cs + f];
+        const double hx = h[f], hy = h[cs + f], hz = h[2 * cs + f];
         const double tx = my * hz - mz * hy;
         const double ty = mz * hx - mx * hz;
         const double tz = mx * hy - my * hx;
@@ -226,14 +228,16 @@ template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_energy(const T* __restrict__ m, const T* __restrict__ hd,
                                                         Geom g, double ku_over_ms2,
                                                         const StepCtl* ctl, double* __restrict__ partial) {
-    const long long n = g.n;
-    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    // cells of this geometry (a slab: its nz local planes, component stride cs, global plane
+    // z0 + k; the +z bond of its last plane reads the halo plane above it)
+    const long long n = g.n, cs = g.cs;
+    const int nx = g.nx, ny = g.ny, nzg = g.nz_g;
     const double ex = ctl->field[0], ey = ctl->field[1], ez = ctl->field[2];
     double loc = 0.0, bonds = 0.0;
     for (long long f = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; f < n;
          f += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const double x = m[f], y = m[n + f], z = m[2 * n + f];
-        const double hx = hd[f], hy = hd[n + f], hz = hd[2 * n + f];
+        const double x = m[f], y = m[cs + f], z = m[2 * cs + f];
+        const double hx = hd[f], hy = hd[cs + f], hz = hd[2 * cs + f];
         const double anis = ku_over_ms2 * (y * y + z * z);
         const double demag = -0.5 * kMu0 * (hx * x + hy * y + hz * z);
         const double zeeman = -kMu0 * (ex * x + ey * y + ez * z);
@@ -241,14 +245,14 @@ __global__ void __launch_bounds__(kRedThreads) k_energy(const T* __restrict__ m,
         const int i = static_cast<int>(f % nx);
         const long long r = f / nx;
         const int j = static_cast<int>(r % ny);
-        const int k = static_cast<int>(r / ny);
+        const int k = g.z0 + static_cast<int>(r / ny);
         auto bond = [&](long long b) {
-            const double dx = double(m[b]) - x, dy = double(m[n + b]) - y, dz = double(m[2 * n + b]) - z;
+            const double dx = double(m[b]) - x, dy = double(m[cs + b]) - y, dz = double(m[2 * cs + b]) - z;
             return dx * dx + dy * dy + dz * dz;
         };
         if (i + 1 < nx) bonds += bond(f + 1);
         if (j + 1 < ny) bonds += bond(f + nx);
-        if (k + 1 < nz) bonds += bond(f + static_cast<long long>(nx) * ny);
+        if (k + 1 < nzg) bonds += bond(f + static_cast<long long>(nx) * ny);
     }
     __shared__ double red[2][kRedThreads / 32];
     loc = warp_sum(loc);
@@ -357,10 +361,10 @@ void launch_sum3(const T* m, long long n, long long cs, double* partial, double*
 }
 
 template <typename T>
-void launch_torque_max(const T* m, const T* h, long long n, unsigned long long* out_bits,
+void launch_torque_max(const T* m, const T* h, long long n, long long cs, unsigned long long* out_bits,
                        cudaStream_t stream) {
     cudaMemsetAsync(out_bits, 0, sizeof(unsigned long long), stream);
-    k_torque_max<T><<<reduce_blocks(n), kRedThreads, 0, stream>>>(m, h, n, out_bits);
+    k_torque_max<T><<<reduce_blocks(n), kRedThreads, 0, stream>>>(m, h, n, cs, out_bits);
     check_launch();
 }
 
@@ -389,7 +393,7 @@ void launch_tensor_octant(double* E, int nx, int ny, int nz, double delta, cudaS
     template void launch_llg<T>(int, const T*, const T*, T*, const Geom&, double, double, StepCtl*, \
                                 double*, cudaStream_t);                                            \
     template void launch_sum3<T>(const T*, long long, long long, double*, double*, cudaStream_t);   \
-    template void launch_torque_max<T>(const T*, const T*, long long, unsigned long long*,          \
+    template void launch_torque_max<T>(const T*, const T*, long long, long long, unsigned long long*, \
                                        cudaStream_t);                                              \
     template void launch_energy<T>(const T*, const T*, const Geom&, double, const StepCtl*,         \
                                    double*, double*, cudaStream_t);

@@ -4,28 +4,34 @@
 // Rank r owns the z-slab [z0, z0+nzl) of M (with one halo plane below and above) and the
 // kx column range [k0, k0+ncols) of the half spectrum. One step:
 //
-//   KX   (prime only)  x-r2c of the slab rows         -> S_loc[kx][c][z_loc][y]   (all Xh kx)
-//   A2A  forward       all-to-all transpose          -> S_col[kx_loc][c][z][y]   (all nz z)
-//   KYZ / KYF,KZ,KYI   y/z FFTs + tensor MAC on the local kx columns (no communication)
-//   A2A  backward                                    -> S_loc
-//   HALO               M planes z0-1 and z0+nzl from the neighbour ranks
+//   KX   (prime only)  x-r2c of the slab rows            -> S_loc[kx][c][z_loc][y]  (all Xh kx)
+//   HALO               M planes z0-1 and z0+nzl from the neighbours          (comm stream)
+//   per column chunk j (the rank's columns split into NCH chunks):
+//     A2A forward  (j) rank q's planes of my chunk-j columns -> recv[q]       (comm stream)
+//     KYZ / KYF,KZ,KYI (j) on the chunk: rows gathered through a RowMap from the receive
+//                  buffers and from my own S_loc, results written back in place (main stream)
+//     A2A backward (j) the results back to their owners' S_loc                (comm stream)
 //   KXS                x-c2r -> local terms + LLG -> x-r2c of M_{t+1} (next step's S_loc)
 //
-// The chunk rank r sends to rank q in the forward transpose is one contiguous range of S_loc
-// (kx in q's columns); it lands in q's S_col as a 2-D strided block (rows (kx, c), each the
-// nzl*ny values of r's planes), placed with cudaMemcpy2DAsync. Exchanges go over NCCL
-// (grouped ncclSend/ncclRecv, ncclAllReduce for <m>); the emulated variant runs every rank on
-// one device with device copies instead, which makes the decomposition testable on one GPU:
-// per-rank kernels are the single-device kernels on sub-grids, so the sharded fields equal
-// the single-device ones bitwise.
+// Chunk j+1's all-to-all runs while chunk j's y/z kernels compute, and chunk j's results go
+// back while chunk j+1 computes (two streams, events between them). There are no pack or
+// placement copies: a rank sends contiguous ranges of its S_loc, receives each peer's planes
+// into one contiguous block per peer, and the y/z kernels read and write those blocks in place
+// through the RowMap (fast.hpp); its own planes never leave S_loc.
 //
-// Peer mode (MMB_SHARD_PEER=1): no transposes. The y/z kernels of rank r read the rows of its
-// kx columns straight from every rank's S_loc and write the results back there (RowMap: plain
-// loads/stores into the peers' memory over NVLink, mapped with CUDA IPC), and the halo planes
-// are copied peer to peer. Two stream-ordered barriers (a one-word ncclAllReduce) per step
-// separate the phases: every rank's KXS has written its S_loc before anyone's y/z reads it,
-// and every y/z write-back has landed before any KXS reads. In emulated mode the same kernels
-// run with all S_loc buffers on one device.
+// Exchanges go through a Transport: grouped ncclSend/ncclRecv between processes (one rank per
+// GPU), or, with every rank in one process on one device (the emulated solver that makes the
+// decomposition testable on one GPU), device copies that pair the k-th send from a to b with
+// the k-th receive posted at b from a. Both run the same posting code, so the emulated tests
+// cover the offsets, counts and buffer placement of the NCCL path. The per-rank kernels are
+// the single-device kernels on sub-grids, so the sharded fields equal the single-device ones
+// bitwise.
+//
+// Peer mode (MMB_SHARD_PEER=1): no all-to-all. The y/z kernels of rank r read the rows of its
+// kx columns straight from every rank's S_loc and write the results back there (RowMap over
+// the peers' memory, mapped with CUDA IPC: plain loads/stores over NVLink), and the halo
+// planes are copied peer to peer. Two stream-ordered barriers (a one-word ncclAllReduce) per
+// step separate the phases.
 #include <nccl.h>
 
 #include <algorithm>
@@ -33,9 +39,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "fast.hpp"
@@ -85,19 +94,87 @@ Geom make_geom(int nx, int ny, int nz, int lz_force) {
     return g;
 }
 
+// ---- point-to-point exchange of one group -------------------------------------------------
+class Transport {
+public:
+    virtual ~Transport() = default;
+    virtual void begin(cudaStream_t s) = 0;
+    virtual void send(int from, int to, const void* buf, size_t bytes) = 0;
+    virtual void recv(int at, int from, void* buf, size_t bytes) = 0;
+    virtual void end() = 0;
+};
+
+// One rank per process: grouped NCCL point-to-point operations on the group's stream.
+class NcclTransport final : public Transport {
+public:
+    explicit NcclTransport(ncclComm_t c) : comm_(c) {}
+    void begin(cudaStream_t s) override {
+        s_ = s;
+        nck(ncclGroupStart(), "ncclGroupStart");
+    }
+    void send(int, int to, const void* buf, size_t bytes) override {
+        if (bytes) nck(ncclSend(buf, bytes, ncclInt8, to, comm_, s_), "ncclSend");
+    }
+    void recv(int, int from, void* buf, size_t bytes) override {
+        if (bytes) nck(ncclRecv(buf, bytes, ncclInt8, from, comm_, s_), "ncclRecv");
+    }
+    void end() override { nck(ncclGroupEnd(), "ncclGroupEnd"); }
+
+private:
+    ncclComm_t comm_;
+    cudaStream_t s_ = nullptr;
+};
+
+// Every rank in this process (emulated): at the end of the group the k-th send from a to b
+// is copied into the k-th receive posted at b from a, on the group's stream.
+class LoopbackTransport final : public Transport {
+public:
+    void begin(cudaStream_t s) override {
+        s_ = s;
+        sends_.clear();
+        recvs_.clear();
+    }
+    void send(int from, int to, const void* buf, size_t bytes) override {
+        if (bytes) sends_[{from, to}].push_back({const_cast<void*>(buf), bytes});
+    }
+    void recv(int at, int from, void* buf, size_t bytes) override {
+        if (bytes) recvs_[{from, at}].push_back({buf, bytes});
+    }
+    void end() override {
+        if (sends_.size() != recvs_.size()) throw std::logic_error("loopback transport: unmatched peers");
+        for (auto& [key, ss] : sends_) {
+            auto it = recvs_.find(key);
+            if (it == recvs_.end() || it->second.size() != ss.size())
+                throw std::logic_error("loopback transport: unmatched send/recv");
+            for (size_t i = 0; i < ss.size(); ++i) {
+                if (ss[i].second != it->second[i].second) throw std::logic_error("loopback transport: size mismatch");
+                ck(cudaMemcpyAsync(it->second[i].first, ss[i].first, ss[i].second, cudaMemcpyDeviceToDevice, s_),
+                   "loopback copy");
+            }
+        }
+    }
+
+private:
+    cudaStream_t s_ = nullptr;
+    std::map<std::pair<int, int>, std::vector<std::pair<void*, size_t>>> sends_, recvs_;
+};
+
 template <typename T>
 struct Rank {
     int rank = 0, z0 = 0, nzl = 0, k0 = 0, ncols = 0;
     Geom gs{}, gc{};              // slab (x phase) / column (y-z phase) geometry
     long long plane = 0;          // nx*ny
     DevBuf<T> mb[2];              // [3][nzl + 2][ny][nx], halo planes first and last
-    DevBuf<cx<T>> s_loc, s_col, s2, stage;
+    DevBuf<T> hb;                 // H (field hooks), same layout as mb
+    DevBuf<cx<T>> s_loc, recv, s2;
+    std::vector<long long> roff;  // recv: start of peer q's block [ncols][3][nzl_q][ny]
     DevBuf<T> kspec;              // tensor slab of the local kx columns [ncols][zh][yh][6]
     DevBuf<cx<T>> twx, twy, twz;
     DevBuf<StepCtl> ctl;
     DevBuf<double> tpart, partial, red;
     int tpart_count = 0;
     T* m(int which) { return mb[which].p + plane; } // plane 0 of the slab, component 0
+    T* h() { return hb.p + plane; }
 };
 
 template <typename T>
@@ -107,6 +184,7 @@ public:
                 const void* nccl_id, bool emulated)
         : d_(d), world_(world), emulated_(emulated) {
         if (world < 1) throw std::invalid_argument("mmb: world size must be >= 1");
+        if (world > kMaxRanks) throw std::invalid_argument("mmb: z-slab sharding supports up to 8 ranks");
         if (d.nx < 1 || d.ny < 1 || d.nz < 1) throw std::invalid_argument("Grid: cell counts must be >= 1");
         if (!(d.delta > 0.0)) throw std::invalid_argument("Grid: cell edge length must be > 0");
         if (!(d.ms > 0.0)) throw std::invalid_argument("MaterialParams: ms must be > 0");
@@ -117,6 +195,7 @@ public:
         set_schedule(stages, nstages);
         ck(cudaSetDevice(d.device), "cudaSetDevice");
         ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
 
         // global geometry and path (fused y/z for nz <= 8, streaming y/z otherwise)
         Geom g = make_geom(d.nx, d.ny, d.nz, 0);
@@ -129,8 +208,19 @@ public:
         if (g_.xh < world) throw std::invalid_argument("mmb: z-slab sharding needs Lx/2+1 >= world size");
         slabs_ = split_range(d.nz, world);
         cols_ = split_range(g_.xh, world);
+        // column chunks of the overlapped exchange (MMB_SHARD_CHUNKS, default 4; 1 = no overlap)
+        nch_ = 4;
+        if (const char* e = std::getenv("MMB_SHARD_CHUNKS"); e && std::atoi(e) > 0) nch_ = std::atoi(e);
+        if (world == 1) nch_ = 1;
+        for (int q = 0; q < world; ++q) {
+            const int nc = cols_[q].second - cols_[q].first;
+            chunks_.push_back(split_range(nc, std::min(nch_, nc)));
+            chunks_.back().resize(nch_, {nc, nc}); // ranks with fewer columns than chunks: empty tail
+        }
         exch_coeff_ = 2.0 * d.a_ex / (kMu0 * d.ms * d.ms * d.delta * d.delta);
         aniso_coeff_ = d.hk / d.ms;
+        const char* pe = std::getenv("MMB_SHARD_PEER");
+        peer_ = pe && pe[0] == '1' && world > 1;
 
         // tensor spectrum for all kx once (fast layout [kx][kz][ky][6]), sliced per rank
         DevBuf<T> kfull;
@@ -138,17 +228,19 @@ public:
 
         if (emulated_) {
             for (int r = 0; r < world; ++r) ranks_.push_back(make_rank(r, kfull));
+            transport_ = std::make_unique<LoopbackTransport>();
         } else {
             ranks_.push_back(make_rank(my_rank, kfull));
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
             nck(ncclCommInitRank(&comm_, world, id, my_rank), "ncclCommInitRank");
+            transport_ = std::make_unique<NcclTransport>(comm_);
         }
-        const char* pe = std::getenv("MMB_SHARD_PEER");
-        peer_ = pe && pe[0] == '1' && world > 1;
-        if (peer_) {
-            if (world > kMaxRanks) throw std::invalid_argument("mmb: peer mode supports up to 8 ranks");
-            setup_peers();
+        if (peer_) setup_peers();
+        for (int i = 0; i < 2 * nch_ + 2; ++i) {
+            cudaEvent_t e;
+            ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            events_.push_back(e);
         }
         prepare_fast_kernels<T>(ranks_[0]->gs);
         if (yz_) prepare_fast_kernels<T>(ranks_[0]->gc);
@@ -182,8 +274,12 @@ public:
             for (void* p : ipc_open_)
                 if (p) cudaIpcCloseMemHandle(p);
         }
+        if (comm_stream_) cudaStreamSynchronize(comm_stream_);
+        if (stream_) cudaStreamSynchronize(stream_);
+        for (auto e : events_) cudaEventDestroy(e);
         if (comm_) ncclCommDestroy(comm_);
         ranks_.clear();
+        if (comm_stream_) cudaStreamDestroy(comm_stream_);
         if (stream_) cudaStreamDestroy(stream_);
     }
 
@@ -200,52 +296,19 @@ public:
     }
 
     void set_m(const void* x, const void* y, const void* z) override {
-        const void* src[3] = {x, y, z};
-        const int zbase = emulated_ ? 0 : ranks_[0]->z0;
-        for (auto& rp : ranks_) {
-            Rank<T>& R = *rp;
-            for (int c = 0; c < 3; ++c)
-                ck(cudaMemcpyAsync(R.m(cur_) + c * R.gs.cs,
-                                   static_cast<const T*>(src[c]) + (R.z0 - zbase) * R.plane,
-                                   R.nzl * R.plane * sizeof(T), cudaMemcpyHostToDevice, stream_), "set_m");
-        }
+        upload([&](Rank<T>& R) { return R.m(cur_); }, x, y, z, "set_m");
         s_valid_ = false;
-        ck(cudaStreamSynchronize(stream_), "set_m sync");
     }
 
     void get_m(void* x, void* y, void* z) override {
-        void* dst[3] = {x, y, z};
-        const int zbase = emulated_ ? 0 : ranks_[0]->z0;
-        for (auto& rp : ranks_) {
-            Rank<T>& R = *rp;
-            for (int c = 0; c < 3; ++c)
-                ck(cudaMemcpyAsync(static_cast<T*>(dst[c]) + (R.z0 - zbase) * R.plane,
-                                   R.m(cur_) + c * R.gs.cs, R.nzl * R.plane * sizeof(T),
-                                   cudaMemcpyDeviceToHost, stream_), "get_m");
-        }
-        sync_and_check();
+        download([&](Rank<T>& R) { return R.m(cur_); }, x, y, z, "get_m");
     }
 
     void step(long long n) override {
-        if (peer_) {
-            step_peer(n);
-            return;
-        }
         for (long long i = 0; i < n; ++i) {
             prime();
-            transpose_forward();
-            for (auto& rp : ranks_) {
-                Rank<T>& R = *rp;
-                if (yz_) {
-                    launch_fast_yz<T>(R.s_col.p, R.gc, R.twy.p, R.kspec.p, R.ctl.p, st_, 1, stream_);
-                } else {
-                    launch_big_yf<T>(R.s_col.p, R.s2.p, R.gc, R.twy.p, R.ctl.p, st_, 1, stream_);
-                    launch_big_z<T>(R.s2.p, R.gc, R.twz.p, R.kspec.p, stream_);
-                    launch_big_yi<T>(R.s2.p, R.s_col.p, R.gc, R.twy.p, stream_);
-                }
-            }
-            transpose_backward();
-            halo_exchange(cur_);
+            if (peer_) exchange_and_yz_peer(1, true);
+            else exchange_and_yz(1, true);
             for (auto& rp : ranks_) {
                 Rank<T>& R = *rp;
                 launch_fast_xstep<T>(R.s_loc.p, R.m(cur_), R.m(cur_ ^ 1), R.gs, R.twx.p, exch_coeff_,
@@ -264,45 +327,22 @@ public:
             Rank<T>& R = *rp;
             launch_sum3<T>(R.m(cur_), R.nzl * R.plane, R.gs.cs, R.partial.p, R.red.p, stream_);
         }
-        if (!emulated_) {
-            Rank<T>& R = *ranks_[0];
-            nck(ncclAllReduce(R.red.p, R.red.p, 3, ncclDouble, ncclSum, comm_, stream_), "ncclAllReduce");
-            ck(cudaMemcpyAsync(s, R.red.p, sizeof(s), cudaMemcpyDeviceToHost, stream_), "average");
-            sync_and_check();
-        } else {
-            for (auto& rp : ranks_) {
-                double t[3];
-                ck(cudaMemcpyAsync(t, rp->red.p, sizeof(t), cudaMemcpyDeviceToHost, stream_), "average");
-                ck(cudaStreamSynchronize(stream_), "average sync");
-                for (int c = 0; c < 3; ++c) s[c] += t[c];
-            }
-            sync_and_check();
-        }
+        reduce_over_ranks(s, 3, ncclSum);
+        sync_and_check();
         const double inv = 1.0 / static_cast<double>(g_.n);
         const double inv_ms = 1.0 / d_.ms;
         for (int c = 0; c < 3; ++c) out[c] = (inv * s[c]) * inv_ms;
     }
 
     double last_torque_sq() override {
-        double best = 0.0;
         for (auto& rp : ranks_) {
             Rank<T>& R = *rp;
             launch_torque_partials(R.tpart.p, R.tpart_count, R.ctl.p, stream_);
-            StepCtl c;
-            ck(cudaMemcpyAsync(&c, R.ctl.p, sizeof(c), cudaMemcpyDeviceToHost, stream_), "ctl");
-            ck(cudaStreamSynchronize(stream_), "ctl sync");
-            double v;
-            std::memcpy(&v, &c.torque_sq_bits, sizeof(v));
-            best = std::max(best, v);
+            ck(cudaMemcpyAsync(R.red.p, &R.ctl.p->torque_sq_bits, sizeof(double), cudaMemcpyDeviceToDevice, stream_),
+               "torque");
         }
-        if (!emulated_) {
-            // max over ranks
-            Rank<T>& R = *ranks_[0];
-            ck(cudaMemcpyAsync(R.red.p, &best, sizeof(best), cudaMemcpyHostToDevice, stream_), "torque");
-            nck(ncclAllReduce(R.red.p, R.red.p, 1, ncclDouble, ncclMax, comm_, stream_), "ncclAllReduce");
-            ck(cudaMemcpyAsync(&best, R.red.p, sizeof(best), cudaMemcpyDeviceToHost, stream_), "torque");
-            ck(cudaStreamSynchronize(stream_), "torque sync");
-        }
+        double best = 0.0;
+        reduce_over_ranks(&best, 1, ncclMax);
         return best;
     }
 
@@ -355,15 +395,29 @@ public:
     }
 
     int launches_per_step() const override {
-        return static_cast<int>(ranks_.size()) * (yz_ ? 2 : 4);
+        // per local rank: the y/z kernels of each non-empty column chunk (one launch per rank
+        // in peer mode), and the x step
+        int k = 0;
+        for (auto& rp : ranks_) {
+            if (peer_) {
+                k += yz_ ? 1 : 3;
+                continue;
+            }
+            for (int j = 0; j < nch_; ++j)
+                if (chunks_[rp->rank][j].second > chunks_[rp->rank][j].first) k += yz_ ? 1 : 3;
+        }
+        return k + static_cast<int>(ranks_.size());
     }
 
     std::string path_info() const override {
-        char head[200];
+        char head[240];
         const Rank<T>& R = *ranks_[0];
-        std::snprintf(head, sizeof head, "path=sharded-%s world=%d mode=%s%s n=%dx%dx%d L=%dx%dx%d prec=%s slab=%d+%d cols=%d+%d",
-                      yz_ ? "yz" : "big", world_, emulated_ ? "emulated" : "nccl", peer_ ? "+peer" : "", d_.nx, d_.ny,
-                      d_.nz, g_.lx, g_.ly, g_.lz, sizeof(T) == 8 ? "f64" : "f32", R.z0, R.nzl, R.k0, R.ncols);
+        std::snprintf(head, sizeof head,
+                      "path=sharded-%s world=%d mode=%s n=%dx%dx%d L=%dx%dx%d prec=%s slab=%d+%d cols=%d+%d chunks=%d",
+                      yz_ ? "yz" : "big", world_,
+                      emulated_ ? (peer_ ? "emulated+peer" : "emulated") : (peer_ ? "nccl+peer" : "nccl"), d_.nx,
+                      d_.ny, d_.nz, g_.lx, g_.ly, g_.lz, sizeof(T) == 8 ? "f64" : "f32", R.z0, R.nzl, R.k0, R.ncols,
+                      peer_ ? 1 : nch_);
         std::string s = head;
         s += "; " + (yz_ ? fast_describe<T>(R.gc) : big_describe<T>(R.gc));
         const std::string x = fast_describe<T>(R.gs);
@@ -375,22 +429,56 @@ public:
         size_t b = 0;
         for (auto& rp : ranks_) {
             const Rank<T>& R = *rp;
-            b += R.mb[0].bytes() + R.mb[1].bytes() + R.s_loc.bytes() + R.s_col.bytes() + R.s2.bytes() +
-                 R.stage.bytes() + R.kspec.bytes() + R.twx.bytes() + R.twy.bytes() + R.twz.bytes() +
-                 R.ctl.bytes() + R.tpart.bytes() + R.partial.bytes() + R.red.bytes();
+            b += R.mb[0].bytes() + R.mb[1].bytes() + R.hb.bytes() + R.s_loc.bytes() + R.recv.bytes() +
+                 R.s2.bytes() + R.kspec.bytes() + R.twx.bytes() + R.twy.bytes() + R.twz.bytes() + R.ctl.bytes() +
+                 R.tpart.bytes() + R.partial.bytes() + R.red.bytes();
         }
         return b;
     }
 
-    // field hooks are single-device features
-    double energy() override { throw std::invalid_argument("mmb: energy() is not available on a sharded handle"); }
-    double max_torque() override { throw std::invalid_argument("mmb: max_torque() is not available on a sharded handle"); }
-    void effective_field(void*, void*, void*) override {
-        throw std::invalid_argument("mmb: effective_field() is not available on a sharded handle");
+    // ---- field hooks on the slabs (collective over the ranks) --------------------------------
+    // Simulation<T>::energy (llg.cpp:133-138): applied field at step_ (no alpha update), demag
+    // recomputed, total_energy (energy.cpp:39-64): local densities and exchange bonds summed
+    // per slab (the +z bonds of a slab's last plane read its halo), then over the ranks.
+    double energy() override {
+        demag_slabs(nullptr, 3, true);
+        const double ms = d_.ms, ku = 0.5 * d_.hk * kMu0 * ms;
+        for (auto& rp : ranks_) {
+            Rank<T>& R = *rp;
+            launch_energy<T>(R.m(cur_), R.h(), R.gs, ku / (ms * ms), R.ctl.p, R.partial.p, R.red.p, stream_);
+        }
+        double e[2] = {0.0, 0.0};
+        reduce_over_ranks(e, 2, ncclSum);
+        sync_and_check();
+        return e[0] * (d_.delta * d_.delta * d_.delta) + d_.a_ex * d_.delta / (ms * ms) * e[1];
     }
-    void demag_field(const void*, const void*, const void*, void*, void*, void*) override {
-        throw std::invalid_argument("mmb: demag_field() is not available on a sharded handle");
+
+    // llg.cpp:140-156: re-assemble H_eff (may apply the sticky alpha override), then the fp64
+    // max of |M x H| over all cells (max over the ranks).
+    double max_torque() override {
+        heff_slabs();
+        for (auto& rp : ranks_) {
+            Rank<T>& R = *rp;
+            launch_torque_max<T>(R.m(cur_), R.h(), R.nzl * R.plane, R.gs.cs,
+                                 reinterpret_cast<unsigned long long*>(R.red.p), stream_);
+        }
+        double sq = 0.0;
+        reduce_over_ranks(&sq, 1, ncclMax);
+        sync_and_check();
+        return std::sqrt(sq) / (d_.ms * d_.ms);
     }
+
+    void effective_field(void* x, void* y, void* z) override {
+        heff_slabs();
+        download([&](Rank<T>& R) { return R.h(); }, x, y, z, "effective_field");
+    }
+
+    void demag_field(const void* mx, const void* my, const void* mz, void* hx, void* hy, void* hz) override {
+        upload([&](Rank<T>& R) { ensure_h(R); return R.h(); }, mx, my, mz, "demag upload");
+        demag_slabs([&](Rank<T>& R) { return R.h(); }, 0, false);
+        download([&](Rank<T>& R) { return R.h(); }, hx, hy, hz, "demag_field");
+    }
+
     void tensor_octant(double*) override {
         throw std::invalid_argument("mmb: tensor_octant() is not available on a sharded handle");
     }
@@ -399,33 +487,230 @@ public:
     }
 
 private:
-    // ---- peer mode -------------------------------------------------------------------------
-    void step_peer(long long n) {
-        for (long long i = 0; i < n; ++i) {
-            prime();
-            barrier(); // every rank's S_loc (KXS / prime output) is complete
-            for (size_t k = 0; k < ranks_.size(); ++k) {
-                Rank<T>& R = *ranks_[k];
-                const RowMap<T>& rm = rowmaps_[k];
-                if (R.ncols == 0) continue;
-                if (yz_) {
-                    launch_fast_yz<T>(R.s_loc.p, R.gc, R.twy.p, R.kspec.p, R.ctl.p, st_, 1, stream_, false, &rm);
+    // ---- host <-> slab copies (the handle's planes: one rank's slab, or all in emulated mode)
+    template <typename F>
+    void upload(F dst_of, const void* x, const void* y, const void* z, const char* what) {
+        const void* src[3] = {x, y, z};
+        const int zbase = emulated_ ? 0 : ranks_[0]->z0;
+        for (auto& rp : ranks_) {
+            Rank<T>& R = *rp;
+            T* dst = dst_of(R);
+            for (int c = 0; c < 3; ++c)
+                ck(cudaMemcpyAsync(dst + c * R.gs.cs, static_cast<const T*>(src[c]) + (R.z0 - zbase) * R.plane,
+                                   R.nzl * R.plane * sizeof(T), cudaMemcpyHostToDevice, stream_), what);
+        }
+        ck(cudaStreamSynchronize(stream_), what);
+    }
+    template <typename F>
+    void download(F src_of, void* x, void* y, void* z, const char* what) {
+        void* dst[3] = {x, y, z};
+        const int zbase = emulated_ ? 0 : ranks_[0]->z0;
+        for (auto& rp : ranks_) {
+            Rank<T>& R = *rp;
+            const T* src = src_of(R);
+            for (int c = 0; c < 3; ++c)
+                ck(cudaMemcpyAsync(static_cast<T*>(dst[c]) + (R.z0 - zbase) * R.plane, src + c * R.gs.cs,
+                                   R.nzl * R.plane * sizeof(T), cudaMemcpyDeviceToHost, stream_), what);
+        }
+        sync_and_check();
+    }
+
+    // v[0..k) of every local rank's red buffer, then over the ranks (NCCL all-reduce on the
+    // main stream, or in rank order on the host for the emulated ranks)
+    void reduce_over_ranks(double* v, int k, ncclRedOp_t op) {
+        for (int i = 0; i < k; ++i) v[i] = 0.0;
+        if (!emulated_) {
+            Rank<T>& R = *ranks_[0];
+            nck(ncclAllReduce(R.red.p, R.red.p, k, ncclDouble, op, comm_, stream_), "ncclAllReduce");
+            ck(cudaMemcpyAsync(v, R.red.p, k * sizeof(double), cudaMemcpyDeviceToHost, stream_), "reduce");
+            ck(cudaStreamSynchronize(stream_), "reduce sync");
+            return;
+        }
+        for (auto& rp : ranks_) {
+            double t[8];
+            ck(cudaMemcpyAsync(t, rp->red.p, k * sizeof(double), cudaMemcpyDeviceToHost, stream_), "reduce");
+            ck(cudaStreamSynchronize(stream_), "reduce sync");
+            for (int i = 0; i < k; ++i) v[i] = op == ncclMax ? std::max(v[i], t[i]) : v[i] + t[i];
+        }
+    }
+
+    void ensure_h(Rank<T>& R) {
+        if (!R.hb.p) {
+            R.hb.alloc(R.mb[0].n);
+            ck(cudaMemsetAsync(R.hb.p, 0, R.hb.bytes(), stream_), "memset");
+        }
+    }
+
+    // H_demag of M (m_of(R) per rank, or M_cur with nullptr) into every rank's H slab;
+    // prologue 2 / 3 as in Solver::enqueue_demag. `halo`: also refresh M_cur's halo planes
+    // (the local terms and the energy's bonds read them).
+    template <typename F>
+    void demag_slabs(F m_of, int prologue, bool halo) {
+        for (auto& rp : ranks_) ensure_h(*rp);
+        for (auto& rp : ranks_) {
+            Rank<T>& R = *rp;
+            const T* m = nullptr;
+            if constexpr (std::is_same_v<F, std::nullptr_t>) m = R.m(cur_);
+            else m = m_of(R);
+            launch_fast_xf<T>(m, R.s_loc.p, R.gs, R.twx.p, R.ctl.p, st_, 0, stream_);
+        }
+        if (peer_) exchange_and_yz_peer(prologue, halo);
+        else exchange_and_yz(prologue, halo);
+        for (auto& rp : ranks_) {
+            Rank<T>& R = *rp;
+            launch_fast_xi<T>(R.s_loc.p, R.h(), R.gs, R.twx.p, stream_);
+        }
+        s_valid_ = false; // S_loc held another spectrum
+    }
+
+    void heff_slabs() {
+        demag_slabs(nullptr, 2, true);
+        for (auto& rp : ranks_) {
+            Rank<T>& R = *rp;
+            // in place: each thread reads its own H_demag cell before writing H_eff there
+            launch_llg<T>(1, R.m(cur_), R.h(), R.h(), R.gs, exch_coeff_, aniso_coeff_, R.ctl.p, R.tpart.p, stream_);
+        }
+    }
+
+    // ---- the all-to-all step phase -----------------------------------------------------------
+    cudaEvent_t ev(int i) { return events_[i]; }
+
+    // Halo planes, then per column chunk: forward exchange, y/z kernels, backward exchange.
+    // Exchanges on the comm stream, kernels on the main stream; returns with the main stream
+    // ordered after the last backward exchange.
+    void exchange_and_yz(int prologue, bool halo) {
+        cudaEvent_t ready = ev(2 * nch_), done = ev(2 * nch_ + 1);
+        ck(cudaEventRecord(ready, stream_), "record");
+        ck(cudaStreamWaitEvent(comm_stream_, ready, 0), "wait");
+        if (halo) halo_exchange(cur_, comm_stream_);
+        for (int j = 0; j < nch_; ++j) {
+            exchange_chunk(j, false);
+            ck(cudaEventRecord(ev(j), comm_stream_), "record");
+        }
+        for (int j = 0; j < nch_; ++j) {
+            ck(cudaStreamWaitEvent(stream_, ev(j), 0), "wait");
+            for (auto& rp : ranks_) yz_chunk(*rp, j, j == 0 ? prologue : 0);
+            ck(cudaEventRecord(ev(nch_ + j), stream_), "record");
+        }
+        for (int j = 0; j < nch_; ++j) {
+            ck(cudaStreamWaitEvent(comm_stream_, ev(nch_ + j), 0), "wait");
+            exchange_chunk(j, true);
+        }
+        ck(cudaEventRecord(done, comm_stream_), "record");
+        ck(cudaStreamWaitEvent(stream_, done, 0), "wait");
+    }
+
+    // Chunk j of the all-to-all. Forward: every rank sends each peer q the contiguous S_loc
+    // range of q's chunk-j columns (its planes of them) and receives each peer's planes of its
+    // own chunk-j columns into that peer's receive block. Backward: the reverse.
+    void exchange_chunk(int j, bool backward) {
+        const long long ny = d_.ny;
+        transport_->begin(comm_stream_);
+        for (auto& rp : ranks_) {
+            Rank<T>& R = *rp;
+            const int a = chunks_[R.rank][j].first, b = chunks_[R.rank][j].second;
+            for (int q = 0; q < world_; ++q) {
+                if (q == R.rank) continue;
+                const int nq = slabs_[q].second - slabs_[q].first;
+                // my S_loc range of q's chunk-j columns
+                const int qa = chunks_[q][j].first, qb = chunks_[q][j].second;
+                cx<T>* mine = R.s_loc.p + (cols_[q].first + qa) * 3 * R.nzl * ny;
+                const size_t mine_bytes = static_cast<size_t>(qb - qa) * 3 * R.nzl * ny * sizeof(cx<T>);
+                // q's planes of my chunk-j columns, in q's receive block
+                cx<T>* theirs = R.recv.p + R.roff[q] + static_cast<long long>(a) * 3 * nq * ny;
+                const size_t theirs_bytes = static_cast<size_t>(b - a) * 3 * nq * ny * sizeof(cx<T>);
+                if (!backward) {
+                    transport_->send(R.rank, q, mine, mine_bytes);
+                    transport_->recv(R.rank, q, theirs, theirs_bytes);
                 } else {
-                    launch_big_yf<T>(R.s_loc.p, R.s2.p, R.gc, R.twy.p, R.ctl.p, st_, 1, stream_, &rm);
-                    launch_big_z<T>(R.s2.p, R.gc, R.twz.p, R.kspec.p, stream_);
-                    launch_big_yi<T>(R.s2.p, R.s_loc.p, R.gc, R.twy.p, stream_, &rm);
+                    transport_->send(R.rank, q, theirs, theirs_bytes);
+                    transport_->recv(R.rank, q, mine, mine_bytes);
                 }
             }
-            barrier(); // every y/z write-back into the S_loc buffers has landed
-            halo_peer(cur_);
-            for (auto& rp : ranks_) {
-                Rank<T>& R = *rp;
-                launch_fast_xstep<T>(R.s_loc.p, R.m(cur_), R.m(cur_ ^ 1), R.gs, R.twx.p, exch_coeff_,
-                                     aniso_coeff_, R.ctl.p, R.tpart.p, stream_);
-            }
-            cur_ ^= 1;
-            ++step_;
         }
+        transport_->end();
+    }
+
+    // rows of rank R's chunk-j columns: its own planes in S_loc, each peer's in its receive block
+    RowMap<T> chunk_rows(Rank<T>& R, int j) {
+        RowMap<T> rm{};
+        const int a = chunks_[R.rank][j].first;
+        rm.world = world_;
+        rm.local = 1;
+        for (int q = 0; q < world_; ++q) {
+            rm.z0[q] = slabs_[q].first;
+            if (q == R.rank) {
+                rm.base[q] = R.s_loc.p;
+                rm.kb[q] = R.k0 + a;
+            } else {
+                rm.base[q] = R.recv.p + R.roff[q];
+                rm.kb[q] = a;
+            }
+        }
+        rm.z0[world_] = d_.nz;
+        return rm;
+    }
+
+    void yz_chunk(Rank<T>& R, int j, int prologue) {
+        const int a = chunks_[R.rank][j].first, b = chunks_[R.rank][j].second;
+        if (b <= a) return;
+        Geom gc = R.gc;
+        gc.xh = b - a;
+        const RowMap<T> rm = chunk_rows(R, j);
+        const size_t per_kx = static_cast<size_t>(g_.zh) * g_.yh * 6;
+        const T* kt = R.kspec.p + a * per_kx;
+        if (yz_) {
+            launch_fast_yz<T>(R.s_loc.p, gc, R.twy.p, kt, R.ctl.p, st_, prologue, stream_, false, &rm);
+        } else {
+            cx<T>* s2 = R.s2.p + static_cast<size_t>(a) * 3 * d_.nz * g_.ly;
+            launch_big_yf<T>(R.s_loc.p, s2, gc, R.twy.p, R.ctl.p, st_, prologue, stream_, &rm);
+            launch_big_z<T>(s2, gc, R.twz.p, kt, stream_);
+            launch_big_yi<T>(s2, R.s_loc.p, gc, R.twy.p, stream_, &rm);
+        }
+    }
+
+    // halo planes of M (buffer `which`) from the neighbouring slabs
+    void halo_exchange(int which, cudaStream_t s) {
+        if (world_ == 1) return;
+        if (peer_) {
+            halo_peer(which, s);
+            return;
+        }
+        const size_t pb = static_cast<size_t>(d_.nx) * d_.ny * sizeof(T);
+        transport_->begin(s);
+        for (auto& rp : ranks_) {
+            Rank<T>& R = *rp;
+            for (int c = 0; c < 3; ++c) {
+                T* mc = R.m(which) + c * R.gs.cs;
+                if (R.rank > 0) {
+                    transport_->send(R.rank, R.rank - 1, mc, pb);
+                    transport_->recv(R.rank, R.rank - 1, mc - R.plane, pb);
+                }
+                if (R.rank + 1 < world_) {
+                    transport_->send(R.rank, R.rank + 1, mc + (R.nzl - 1) * R.plane, pb);
+                    transport_->recv(R.rank, R.rank + 1, mc + R.nzl * R.plane, pb);
+                }
+            }
+        }
+        transport_->end();
+    }
+
+    // ---- peer mode -------------------------------------------------------------------------
+    void exchange_and_yz_peer(int prologue, bool halo) {
+        barrier(); // every rank's S_loc (KXS / prime output) is complete
+        for (size_t k = 0; k < ranks_.size(); ++k) {
+            Rank<T>& R = *ranks_[k];
+            const RowMap<T>& rm = rowmaps_[k];
+            if (yz_) {
+                launch_fast_yz<T>(R.s_loc.p, R.gc, R.twy.p, R.kspec.p, R.ctl.p, st_, prologue, stream_, false, &rm);
+            } else {
+                launch_big_yf<T>(R.s_loc.p, R.s2.p, R.gc, R.twy.p, R.ctl.p, st_, prologue, stream_, &rm);
+                launch_big_z<T>(R.s2.p, R.gc, R.twz.p, R.kspec.p, stream_);
+                launch_big_yi<T>(R.s2.p, R.s_loc.p, R.gc, R.twy.p, stream_, &rm);
+            }
+        }
+        barrier(); // every y/z write-back into the S_loc buffers has landed
+        if (halo) halo_peer(cur_, stream_);
     }
 
     // stream-ordered barrier across ranks (nothing to do when all ranks share one stream)
@@ -484,9 +769,10 @@ private:
         for (auto& rp : ranks_) {
             RowMap<T> rm{};
             rm.world = world_;
-            rm.k0 = rp->k0;
+            rm.local = emulated_ ? 1 : 0;
             for (int q = 0; q < world_; ++q) {
                 rm.base[q] = s_loc_of_[q];
+                rm.kb[q] = rp->k0;
                 rm.z0[q] = slabs_[q].first;
             }
             rm.z0[world_] = d_.nz;
@@ -494,8 +780,8 @@ private:
         }
     }
 
-    // halo planes of M_cur copied from the neighbours' slabs (peer to peer)
-    void halo_peer(int which) {
+    // halo planes of M copied from the neighbours' slabs (peer to peer)
+    void halo_peer(int which, cudaStream_t s) {
         const size_t plane = static_cast<size_t>(d_.nx) * d_.ny, pb = plane * sizeof(T);
         for (auto& rp : ranks_) {
             Rank<T>& R = *rp;
@@ -504,12 +790,12 @@ private:
                 if (R.rank > 0) {
                     const int q = R.rank - 1, nq = slabs_[q].second - slabs_[q].first;
                     const T* src = m_of_[which][q] + plane + c * (nq + 2) * plane + (nq - 1) * plane;
-                    ck(cudaMemcpyAsync(mc - plane, src, pb, cudaMemcpyDefault, stream_), "halo (peer)");
+                    ck(cudaMemcpyAsync(mc - plane, src, pb, cudaMemcpyDefault, s), "halo (peer)");
                 }
                 if (R.rank + 1 < world_) {
                     const int q = R.rank + 1, nq = slabs_[q].second - slabs_[q].first;
                     const T* src = m_of_[which][q] + plane + c * (nq + 2) * plane;
-                    ck(cudaMemcpyAsync(mc + R.nzl * plane, src, pb, cudaMemcpyDefault, stream_), "halo (peer)");
+                    ck(cudaMemcpyAsync(mc + R.nzl * plane, src, pb, cudaMemcpyDefault, s), "halo (peer)");
                 }
             }
         }
@@ -595,9 +881,15 @@ private:
         R->mb[0].alloc(3 * (R->nzl + 2) * plane);
         R->mb[1].alloc(3 * (R->nzl + 2) * plane);
         R->s_loc.alloc(static_cast<size_t>(g_.xh) * 3 * R->nzl * d_.ny);
-        R->s_col.alloc(static_cast<size_t>(std::max(R->ncols, 1)) * 3 * d_.nz * d_.ny);
+        // receive blocks: peer q's planes of my columns [ncols][3][nzl_q][ny], q != r
+        R->roff.assign(world_, 0);
+        long long off = 0;
+        for (int q = 0; q < world_; ++q) {
+            R->roff[q] = off;
+            if (q != r) off += static_cast<long long>(R->ncols) * 3 * (slabs_[q].second - slabs_[q].first) * d_.ny;
+        }
+        if (!peer_) R->recv.alloc(static_cast<size_t>(std::max(off, 1LL)));
         if (!yz_) R->s2.alloc(static_cast<size_t>(std::max(R->ncols, 1)) * 3 * d_.nz * g_.ly);
-        if (!emulated_) R->stage.alloc(std::max(R->s_loc.n, R->s_col.n));
         const size_t per_kx = static_cast<size_t>(g_.zh) * g_.yh * 6;
         R->kspec.alloc(std::max(R->ncols, 1) * per_kx);
         if (R->ncols > 0)
@@ -633,135 +925,6 @@ private:
         for (auto& rp : ranks_)
             launch_fast_xf<T>(rp->m(cur_), rp->s_loc.p, rp->gs, rp->twx.p, rp->ctl.p, st_, 0, stream_);
         s_valid_ = true;
-    }
-
-    // element offsets and counts of the transposes (complex elements)
-    long long loc_chunk_off(int nzl_r, int q) const { return static_cast<long long>(cols_[q].first) * 3 * nzl_r * d_.ny; }
-    long long loc_chunk_cnt(int nzl_r, int q) const {
-        return static_cast<long long>(cols_[q].second - cols_[q].first) * 3 * nzl_r * d_.ny;
-    }
-
-    void copy2d(cx<T>* dst, size_t dpitch, const cx<T>* src, size_t spitch, size_t width, size_t height) {
-        if (width == 0 || height == 0) return;
-        ck(cudaMemcpy2DAsync(dst, dpitch * sizeof(cx<T>), src, spitch * sizeof(cx<T>), width * sizeof(cx<T>),
-                             height, cudaMemcpyDeviceToDevice, stream_), "cudaMemcpy2DAsync");
-    }
-
-    // S_loc (all kx, local planes) -> S_col (local kx, all planes)
-    void transpose_forward() {
-        const size_t ny = d_.ny, nz = d_.nz;
-        if (emulated_) {
-            for (auto& rp : ranks_)
-                for (auto& qp : ranks_) {
-                    Rank<T>& R = *rp;
-                    Rank<T>& Q = *qp;
-                    // R's planes for Q's columns -> Q.s_col rows (kx, c), plane offset R.z0
-                    copy2d(Q.s_col.p + R.z0 * ny, nz * ny, R.s_loc.p + loc_chunk_off(R.nzl, Q.rank),
-                           R.nzl * ny, R.nzl * ny, static_cast<size_t>(Q.ncols) * 3);
-                }
-            return;
-        }
-        Rank<T>& R = *ranks_[0];
-        // receive every peer's chunk contiguously into `stage`, then place it
-        std::vector<long long> roff(world_);
-        long long off = 0;
-        for (int q = 0; q < world_; ++q) {
-            roff[q] = off;
-            off += static_cast<long long>(R.ncols) * 3 * (slabs_[q].second - slabs_[q].first) * d_.ny;
-        }
-        nck(ncclGroupStart(), "ncclGroupStart");
-        for (int q = 0; q < world_; ++q) {
-            if (q == R.rank) continue;
-            const long long sc = loc_chunk_cnt(R.nzl, q);
-            if (sc) nck(ncclSend(R.s_loc.p + loc_chunk_off(R.nzl, q), 2 * sc * sizeof(T), ncclInt8, q, comm_, stream_), "ncclSend");
-            const long long rc = static_cast<long long>(R.ncols) * 3 * (slabs_[q].second - slabs_[q].first) * d_.ny;
-            if (rc) nck(ncclRecv(R.stage.p + roff[q], 2 * rc * sizeof(T), ncclInt8, q, comm_, stream_), "ncclRecv");
-        }
-        nck(ncclGroupEnd(), "ncclGroupEnd");
-        for (int q = 0; q < world_; ++q) {
-            const int zq = slabs_[q].first, nq = slabs_[q].second - slabs_[q].first;
-            const cx<T>* src = (q == R.rank) ? R.s_loc.p + loc_chunk_off(R.nzl, q) : R.stage.p + roff[q];
-            copy2d(R.s_col.p + zq * ny, nz * ny, src, nq * ny, nq * ny, static_cast<size_t>(R.ncols) * 3);
-        }
-    }
-
-    // S_col -> S_loc
-    void transpose_backward() {
-        const size_t ny = d_.ny, nz = d_.nz;
-        if (emulated_) {
-            for (auto& rp : ranks_)
-                for (auto& qp : ranks_) {
-                    Rank<T>& R = *rp; // holds columns
-                    Rank<T>& Q = *qp; // receives its planes of R's columns
-                    copy2d(Q.s_loc.p + loc_chunk_off(Q.nzl, R.rank), Q.nzl * ny, R.s_col.p + Q.z0 * ny, nz * ny,
-                           Q.nzl * ny, static_cast<size_t>(R.ncols) * 3);
-                }
-            return;
-        }
-        Rank<T>& R = *ranks_[0];
-        // pack each peer's planes of my columns contiguously, then exchange
-        std::vector<long long> soff(world_);
-        long long off = 0;
-        for (int q = 0; q < world_; ++q) {
-            const int zq = slabs_[q].first, nq = slabs_[q].second - slabs_[q].first;
-            soff[q] = off;
-            if (q != R.rank)
-                copy2d(R.stage.p + off, nq * ny, R.s_col.p + zq * ny, nz * ny, nq * ny, static_cast<size_t>(R.ncols) * 3);
-            else
-                copy2d(R.s_loc.p + loc_chunk_off(R.nzl, R.rank), R.nzl * ny, R.s_col.p + zq * ny, nz * ny,
-                       R.nzl * ny, static_cast<size_t>(R.ncols) * 3);
-            off += static_cast<long long>(R.ncols) * 3 * nq * d_.ny;
-        }
-        nck(ncclGroupStart(), "ncclGroupStart");
-        for (int q = 0; q < world_; ++q) {
-            if (q == R.rank) continue;
-            const int nq = slabs_[q].second - slabs_[q].first;
-            const long long sc = static_cast<long long>(R.ncols) * 3 * nq * d_.ny;
-            if (sc) nck(ncclSend(R.stage.p + soff[q], 2 * sc * sizeof(T), ncclInt8, q, comm_, stream_), "ncclSend");
-            const long long rc = loc_chunk_cnt(R.nzl, q);
-            if (rc) nck(ncclRecv(R.s_loc.p + loc_chunk_off(R.nzl, q), 2 * rc * sizeof(T), ncclInt8, q, comm_, stream_),
-                        "ncclRecv");
-        }
-        nck(ncclGroupEnd(), "ncclGroupEnd");
-    }
-
-    // halo planes of M_cur from the neighbouring slabs
-    void halo_exchange(int which) {
-        if (world_ == 1) return;
-        const size_t pb = static_cast<size_t>(d_.nx) * d_.ny * sizeof(T);
-        if (emulated_) {
-            for (size_t r = 0; r < ranks_.size(); ++r) {
-                Rank<T>& R = *ranks_[r];
-                for (int c = 0; c < 3; ++c) {
-                    T* mc = R.m(which) + c * R.gs.cs;
-                    if (r > 0) {
-                        Rank<T>& L = *ranks_[r - 1];
-                        ck(cudaMemcpyAsync(mc - R.plane, L.m(which) + c * L.gs.cs + (L.nzl - 1) * L.plane, pb,
-                                           cudaMemcpyDeviceToDevice, stream_), "halo");
-                    }
-                    if (r + 1 < ranks_.size()) {
-                        Rank<T>& U = *ranks_[r + 1];
-                        ck(cudaMemcpyAsync(mc + R.nzl * R.plane, U.m(which) + c * U.gs.cs, pb,
-                                           cudaMemcpyDeviceToDevice, stream_), "halo");
-                    }
-                }
-            }
-            return;
-        }
-        Rank<T>& R = *ranks_[0];
-        nck(ncclGroupStart(), "ncclGroupStart");
-        for (int c = 0; c < 3; ++c) {
-            T* mc = R.m(which) + c * R.gs.cs;
-            if (R.rank > 0) {
-                nck(ncclSend(mc, pb, ncclInt8, R.rank - 1, comm_, stream_), "ncclSend");
-                nck(ncclRecv(mc - R.plane, pb, ncclInt8, R.rank - 1, comm_, stream_), "ncclRecv");
-            }
-            if (R.rank + 1 < world_) {
-                nck(ncclSend(mc + (R.nzl - 1) * R.plane, pb, ncclInt8, R.rank + 1, comm_, stream_), "ncclSend");
-                nck(ncclRecv(mc + R.nzl * R.plane, pb, ncclInt8, R.rank + 1, comm_, stream_), "ncclRecv");
-            }
-        }
-        nck(ncclGroupEnd(), "ncclGroupEnd");
     }
 
     // The first zero-|M| cell over all ranks (keys are (step << 36) | global cell, so the
@@ -803,6 +966,7 @@ private:
     }
 
     void sync_and_check() {
+        ck(cudaStreamSynchronize(comm_stream_), "sync");
         ck(cudaStreamSynchronize(stream_), "sync");
         check_numerical();
     }
@@ -814,8 +978,12 @@ private:
     bool yz_ = false;
     StageTable st_{};
     std::vector<std::pair<int, int>> slabs_, cols_;
+    int nch_ = 1;
+    std::vector<std::vector<std::pair<int, int>>> chunks_; // [rank][chunk] local column range
     std::vector<std::unique_ptr<Rank<T>>> ranks_;
-    cudaStream_t stream_ = nullptr;
+    std::unique_ptr<Transport> transport_;
+    cudaStream_t stream_ = nullptr, comm_stream_ = nullptr;
+    std::vector<cudaEvent_t> events_;
     ncclComm_t comm_ = nullptr;
     bool peer_ = false;
     std::vector<RowMap<T>> rowmaps_;        // per local rank (peer mode)

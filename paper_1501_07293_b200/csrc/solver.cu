@@ -261,7 +261,7 @@ public:
     double max_torque() override {
         // llg.cpp:140-156: re-assemble H_eff (may apply the sticky alpha override).
         enqueue_heff();
-        launch_torque_max<T>(m_[cur_].p, heff_.p, g_.n,
+        launch_torque_max<T>(m_[cur_].p, heff_.p, g_.n, g_.n,
                              reinterpret_cast<unsigned long long*>(red_.p + 4), stream_);
         double sq;
         ck(cudaMemcpyAsync(&sq, red_.p + 4, sizeof(sq), cudaMemcpyDeviceToHost, stream_), "torque");

@@ -153,6 +153,64 @@ def transpose_backward(p: SlabPlan, rank: int, s_cols, group=None):
     return out
 
 
+# ------------------------------------------------------------------ chunked zero-copy exchange
+# Mirror of csrc/shard.cu's default exchange (ShardSolver::exchange_chunk / chunk_rows): each
+# rank's kx columns are split into `nch` chunks; in chunk j every rank sends each peer q the
+# contiguous S_local range of q's chunk-j columns and receives each peer's planes of its own
+# chunk-j columns into that peer's receive block [ncols][3][nslab_q][R] (no packing, no
+# placement); the y/z kernels read and write rows in place through the row map below.
+def column_chunks(p: SlabPlan, nch: int) -> List[List[Tuple[int, int]]]:
+    """[rank][chunk] local column range; ranks with fewer columns than chunks get empty tails."""
+    out = []
+    for q in range(p.world):
+        nc = p.ncols(q)
+        ch = _split(nc, min(nch, nc)) if nc else []
+        out.append(ch + [(nc, nc)] * (nch - len(ch)))
+    return out
+
+
+def recv_offsets(p: SlabPlan, r: int) -> List[int]:
+    """Start (complex elements) of peer q's block in rank r's receive buffer (q != r)."""
+    off, out = 0, []
+    for q in range(p.world):
+        out.append(off)
+        if q != r:
+            off += p.ncols(r) * 3 * p.nslab(q) * p.rows_per_plane()
+    return out
+
+
+def chunk_exchange_ops(p: SlabPlan, r: int, j: int, nch: int):
+    """Rank r's point-to-point operations of chunk j's forward exchange: per peer q,
+    (q, (start, count) in r's S_local sent to q, (start, count) in r's receive buffer filled by
+    q). The backward exchange sends the second range and receives into the first."""
+    ch = column_chunks(p, nch)
+    R = p.rows_per_plane()
+    roff = recv_offsets(p, r)
+    a, b = ch[r][j]
+    ops = []
+    for q in range(p.world):
+        if q == r:
+            continue
+        qa, qb = ch[q][j]
+        send = ((p.cols[q][0] + qa) * 3 * p.nslab(r) * R, (qb - qa) * 3 * p.nslab(r) * R)
+        recv = (roff[q] + a * 3 * p.nslab(q) * R, (b - a) * 3 * p.nslab(q) * R)
+        ops.append((q, send, recv))
+    return ops
+
+
+def chunk_row(p: SlabPlan, r: int, j: int, nch: int, kx: int, c: int, z: int) -> Tuple[str, int]:
+    """Where row (kx, c, z) of rank r's chunk-j launch lives (RowMap::row of chunk_rows):
+    ("s_local", offset) for r's own planes, ("recv", offset) for a peer's."""
+    a = column_chunks(p, nch)[r][j][0]
+    q = 0
+    while z >= p.slabs[q][1]:
+        q += 1
+    z0, R = p.slabs[q][0], p.rows_per_plane()
+    if q == r:
+        return "s_local", ((p.cols[r][0] + a + kx) * 3 + c) * p.nslab(r) * R + (z - z0) * R
+    return "recv", recv_offsets(p, r)[q] + (((a + kx) * 3 + c) * p.nslab(q) + (z - z0)) * R
+
+
 # ------------------------------------------------------------------ peer-memory mode
 def peer_row(p: SlabPlan, rank: int, kx_local: int, c: int, z: int) -> Tuple[int, int]:
     """Where row (kx_local, c, z) of rank `rank`'s columns lives in peer mode (MMB_SHARD_PEER,
