@@ -22,6 +22,9 @@
 #include "llg_cell.cuh"
 #include "fast_common.cuh"
 
+#ifndef MMB_YZ_KPREFETCH
+#define MMB_YZ_KPREFETCH 1 // k_yz (nz > 1): load a pencil's tensor coefficients before its z-DFTs
+#endif
 #ifndef MMB_XS_ZC
 #define MMB_XS_ZC 4 // planes per chunk of the 2-row-tile x grid
 #endif
@@ -354,7 +357,13 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
                 base[RP] = b;
                 base[2 * RP] = cc;
             } else {
-                // 2 <= nz <= 8, Lz = 16
+                // 2 <= nz <= 8, Lz = 16. The pencil's 9 x 6 tensor coefficients are loaded
+                // first, so their global-load latency hides behind the forward z-DFTs.
+                T kk[9][6];
+#if MMB_YZ_KPREFETCH
+#pragma unroll
+                for (int kzo = 0; kzo <= 8; ++kzo) load6<T>(kb + kzo * yh * 6, kk[kzo]);
+#endif
                 cx<T> w[3][16];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
@@ -366,7 +375,12 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
 #pragma unroll
                 for (int kzo = 0; kzo <= 8; ++kzo) {
                     T k6[6];
+#if MMB_YZ_KPREFETCH
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) k6[q] = kk[kzo][q];
+#else
                     load6<T>(kb + kzo * yh * 6, k6);
+#endif
                     if (fy) {
                         k6[1] = -k6[1];
                         k6[4] = -k6[4];

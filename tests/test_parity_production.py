@@ -42,8 +42,8 @@ OUT = os.path.join(os.path.dirname(HERE), "gpurun_out")
 # north-star field gate, and the gates of the step comparisons (measured on B200: see
 # profiles/parity_production_r2.json for the observed values of every case)
 TOL_H = {"f64": 1e-12, "f32": 1e-5}
-TOL_DM = {"f64": 1e-9, "f32": 1e-4}
-TOL_M3 = {"f64": 1e-10, "f32": 1e-4}
+TOL_DM = {"f64": 1e-11, "f32": 2e-5}
+TOL_M3 = {"f64": 1e-12, "f32": 2e-6}
 
 SCHED = [(0, 2, (10.0, -20.0, 5.0)), (2, 10, (0.0, 50.0, 0.0), True, (40.0, 0.0, 0.0), 0.1)]
 
@@ -125,7 +125,20 @@ def test_production_variant_matches_reference(refsolver, case, monkeypatch):
 
     # H_demag of the random state (the y/z kernel of this geometry)
     h_ref = refsolver.heff(ref_problem(refsolver, sp), m0, parts=1)
-    obs["h_demag"] = rel(sim.demag_field(m0), h_ref)
+    h_b = sim.demag_field(m0)
+    obs["h_demag"] = rel(h_b, h_ref)
+    if prec == "f64":
+        # The reference evaluates the prism sums at negative offsets separately, so its tensor
+        # is symmetric only up to the far-field cancellation error of each entry; on grids of
+        # 1e5+ cells that asymmetry alone moves its field by up to ~1e-10 relative (8.4e-11 at
+        # 100x300x12, measured on the CPU: reference vs the reference with its own tensor
+        # symmetrized). The B200 spectrum is exactly symmetric, so the 1e-12 gate is taken
+        # against the reference's convolution of its own tensor symmetrized, and against the
+        # reference itself up to that measured asymmetry.
+        from .test_parity_gpu import _symmetrized_reference_field
+        sym = _symmetrized_reference_field(refsolver.build_tensor(nx, ny, nz, delta), m0, nx, ny, nz)
+        obs["h_demag_vs_symmetrized_ref"] = rel(h_b, sym)
+        obs["ref_tensor_asymmetry"] = rel(sym, h_ref)
 
     # one fused step: the update dM
     sim.set_magnetization(m0)
@@ -150,7 +163,11 @@ def test_production_variant_matches_reference(refsolver, case, monkeypatch):
                             refsolver.heff(ref_problem(refsolver, sp), r.get_m(), sp.schedule.at(3)[0]))
     _observed[case] = obs
 
-    assert obs["h_demag"] <= TOL_H[prec], obs
+    if prec == "f64":
+        assert obs["h_demag_vs_symmetrized_ref"] <= TOL_H[prec], obs
+        assert obs["h_demag"] <= max(TOL_H[prec], obs["ref_tensor_asymmetry"] + TOL_H[prec]), obs
+    else:
+        assert obs["h_demag"] <= TOL_H[prec], obs
     assert obs["heff_step3"] <= TOL_H[prec], obs
     assert obs["dm_step1"] <= TOL_DM[prec], obs
     assert obs["m_step3"] <= TOL_M3[prec], obs

@@ -18,7 +18,7 @@ a = ap.parse_args()
 nx, ny, nz, delta, a_ex, ms, hk, alpha, dt, prec = WORKLOADS[a.workload]
 spec = ProblemSpec(name=a.workload, grid=Grid(nx, ny, nz, delta), material=MaterialParams(a_ex, ms, hk, alpha), dt=dt)
 sim = make_simulation(spec, precision=Precision.f32 if prec == "f32" else Precision.f64)
-sim.set_magnetization(random_state(nx, ny, nz, ms, np.float32 if prec == "f32" else np.float64))
+sim.set_magnetization(random_state(nx, ny, nz, ms, prec))
 sim.time_steps(3)
 t = sim.time_steps(a.steps) / a.steps
 prof = sim.profile_step(a.steps)

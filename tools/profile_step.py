@@ -20,7 +20,7 @@ a = ap.parse_args()
 nx, ny, nz, delta, a_ex, ms, hk, alpha, dt, prec = WORKLOADS[a.workload]
 spec = ProblemSpec(name=a.workload, grid=Grid(nx, ny, nz, delta), material=MaterialParams(a_ex, ms, hk, alpha), dt=dt)
 sim = make_simulation(spec, precision=Precision.f32 if prec == "f32" else Precision.f64)
-sim.set_magnetization(random_state(nx, ny, nz, ms, np.float32 if prec == "f32" else np.float64))
+sim.set_magnetization(random_state(nx, ny, nz, ms, prec))
 sim.step(a.steps)
 sim.synchronize()
 print("ok", a.workload, sim.launches_per_step(), "launches/step")
