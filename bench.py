@@ -355,7 +355,8 @@ def run_b200_sharded(args, world, rank, local):
                 "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
                 "config": {"workload": wl, "nx": nx, "ny": ny, "nz": nz, "delta_nm": delta,
-                           "parallelism": (f"z-slabs x{world} (NCCL all-to-all transposes + halo)" if world > 1
+                           "parallelism": (f"z-slabs x{world} (chunked NCCL all-to-all overlapped with the y/z "
+                                           "kernels, NCCL halo planes)" if world > 1
                                            else "single GPU (one slab: no exchange)"),
                            "l2": "working set >> 126 MB L2; no flush", "cells": n},
                 "roofline": {"bound": "hbm", "kernel": "sharded_step", "achieved": achieved / world,
@@ -368,7 +369,7 @@ def run_b200_sharded(args, world, rank, local):
                         "d2h_bytes_per_step": slab_bytes * world,
                         "api": "mmb_set_m + mmb_step(1) + mmb_get_m per step on every rank's slab"},
                 "gpu_launches": sim.launches_per_step() * args.steps,
-                "clocks": clk.summary(), "device_bytes": sim.device_bytes()}
+                "clocks": clk.summary(), "device_bytes": sim.device_bytes(), "path": sim.path_info()}
         print(json.dumps(line), flush=True)
     barrier(world)
     return 0
@@ -465,7 +466,7 @@ def run_b200(args, world, rank, local):
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": sim.launches_per_step() * args.steps,
                 "clocks": clk.summary(),
-                "device_bytes": sim.device_bytes()}
+                "device_bytes": sim.device_bytes(), "path": sim.path_info()}
         print(json.dumps(line), flush=True)
     barrier(world)
     return 0

@@ -649,6 +649,9 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     cl.load(ctl, coeff, kan);
     double tmax = 0.0;
     const int sy = nx, sz = nx * ny;
+    // 32-bit element indices (3 cs < 2^31) off one base: one 64-bit address per load instead
+    // of 64-bit index arithmetic
+    const int csi = static_cast<int>(cs);
     // walk the tile's cells with a fixed stride, carrying (yl, i) instead of dividing
     int yl = 0, i = tid;
     while (i >= nx) {
@@ -663,15 +666,15 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
         T mc[3], ex[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const T* p = m + c * cs + f;
+            const int q = c * csi + f;
             T nb[6];
-            nb[0] = (mask & 1u) ? __ldg(p - 1) : T(0);
-            nb[1] = (mask & 2u) ? __ldg(p + 1) : T(0);
-            nb[2] = (mask & 4u) ? __ldg(p - sy) : T(0);
-            nb[3] = (mask & 8u) ? __ldg(p + sy) : T(0);
-            nb[4] = (mask & 16u) ? __ldg(p - sz) : T(0);
-            nb[5] = (mask & 32u) ? __ldg(p + sz) : T(0);
-            mc[c] = __ldg(p);
+            nb[0] = (mask & 1u) ? __ldg(m + (q - 1)) : T(0);
+            nb[1] = (mask & 2u) ? __ldg(m + (q + 1)) : T(0);
+            nb[2] = (mask & 4u) ? __ldg(m + (q - sy)) : T(0);
+            nb[3] = (mask & 8u) ? __ldg(m + (q + sy)) : T(0);
+            nb[4] = (mask & 16u) ? __ldg(m + (q - sz)) : T(0);
+            nb[5] = (mask & 32u) ? __ldg(m + (q + sz)) : T(0);
+            mc[c] = __ldg(m + q);
             ex[c] = exch_sum6<T>(mc[c], nb, mask);
         }
         T hx = hm[(0 * TR + yl) * nx + i], hy = hm[(1 * TR + yl) * nx + i], hz = hm[(2 * TR + yl) * nx + i];
@@ -683,7 +686,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
                                          static_cast<unsigned long long>(f + static_cast<long long>(g.z0) * sz));
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            mout[c * cs + f] = mc[c];
+            mout[c * csi + f] = mc[c];
             hm[(c * TR + yl) * nx + i] = mc[c];
         }
         i += NT;
