@@ -42,7 +42,9 @@ OUT = os.path.join(os.path.dirname(HERE), "gpurun_out")
 # north-star field gate, and the gates of the step comparisons (measured on B200: see
 # profiles/parity_production_r2.json for the observed values of every case)
 TOL_H = {"f64": 1e-12, "f32": 1e-5}
-TOL_DM = {"f64": 1e-11, "f32": 2e-5}
+# dM in f32 carries the rounding of M itself (ulp(ms) ~ 6e-5 at ms = 800-1000 against |dM| of
+# a few ms): observed up to 1.5e-5 (256^2 film), 3.3e-6 elsewhere
+TOL_DM = {"f64": 1e-11, "f32": 1e-4}
 TOL_M3 = {"f64": 1e-12, "f32": 2e-6}
 
 SCHED = [(0, 2, (10.0, -20.0, 5.0)), (2, 10, (0.0, 50.0, 0.0), True, (40.0, 0.0, 0.0), 0.1)]
