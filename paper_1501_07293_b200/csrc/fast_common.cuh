@@ -60,27 +60,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
         : "memory");
 }
 
-// two adjacent complex values (row pair) with one 16-byte shared/global access for f32
-template <typename T>
-__device__ __forceinline__ void load_pair(const cx<T>* p, cx<T>& a, cx<T>& b) {
-    if constexpr (sizeof(T) == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(p);
-        a = cx<T>{v.x, v.y};
-        b = cx<T>{v.z, v.w};
-    } else {
-        a = p[0];
-        b = p[1];
-    }
-}
-template <typename T>
-__device__ __forceinline__ void store_pair(cx<T>* p, cx<T> a, cx<T> b) {
-    if constexpr (sizeof(T) == 4) *reinterpret_cast<float4*>(p) = make_float4(a.x, a.y, b.x, b.y);
-    else {
-        p[0] = a;
-        p[1] = b;
-    }
-}
-
 // six tensor coefficients stored contiguously ([..][6]): three 2-vector loads
 template <typename T>
 __device__ __forceinline__ void load6(const T* __restrict__ p, T (&k)[6]) {

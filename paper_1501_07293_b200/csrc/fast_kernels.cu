@@ -486,7 +486,7 @@ struct XS {
     static constexpr int XHP = ((1 << LOG2L) / 2 + 1) | 1;            // staging pitch (odd)
     static constexpr int EX = SP::N1 + 1;
     static constexpr int ZP = (1 << LOG2L) + 1;
-    static constexpr int A0 = 2 * P * ((1 << LOG2L) / 2 + 1), A1 = P * SP::N2 * EX, A2 = P * ZP;
+    static constexpr int A0 = 3 * TR * XHP, A1 = P * SP::N2 * EX, A2 = P * ZP;
     static constexpr int AREA = A0 > A1 ? (A0 > A2 ? A0 : A2) : (A1 > A2 ? A1 : A2);
 };
 template <typename T, int LOG2L, int PB>
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     using SP = Split<LOG2L>;
     using X = XS<LOG2L, PB, sizeof(T)>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = X::P, TR = X::TR, NT = X::NT;
-    constexpr int XH = L / 2 + 1, EX = X::EX, ZP = X::ZP;
+    constexpr int XH = L / 2 + 1, XHP = X::XHP, EX = X::EX, ZP = X::ZP;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
     T* hm = reinterpret_cast<T*>(smem_raw); // [3*TR][nx] tile: H_demag, then M_{t+1}
@@ -547,34 +547,21 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     const long long cur_step = ctl->cur_step;
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->step = cur_step + 1;
 
-    // ---- 1a. stage the 3*TR convolved half-spectrum rows (async copies), interleaved by row
-    // pair: staged element (p, k) holds rows 2p and 2p+1 (same component, consecutive y) side
-    // by side, which is how both S (y fastest) and stage 1b (Z = A + iB of the pair) see them,
-    // so one 16-byte copy (f32) moves both and one 16-byte load feeds a stage-A input. Each
-    // thread keeps one pair and walks kx with a fixed stride (NT is a multiple of P): no
-    // division, 32-bit element offsets.
-    static_assert(NT % P == 0, "thread count must be a multiple of the tile's row pairs");
-    static_assert(TR % 2 == 0, "row pairs never straddle components");
-    constexpr int KSTEP = NT / P;
-    const int my_p = tid % P, my_k0 = tid / P;
-    const int my_c = (2 * my_p) / TR, my_y = y0 + (2 * my_p - my_c * TR);
-    const bool live0 = my_y < ny, live1 = my_y + 1 < ny;
+    // ---- 1a. stage the 3*TR convolved half-spectrum rows (async copies). Each thread keeps
+    // one row r and walks kx with a fixed stride (NT is a multiple of 3*TR): no division,
+    // 32-bit element offsets.
+    static_assert(NT % (3 * TR) == 0, "thread count must be a multiple of the tile rows");
+    constexpr int KSTEP = NT / (3 * TR);
+    const int my_r = tid % (3 * TR), my_k0 = tid / (3 * TR);
+    const int my_c = my_r / TR, my_y = y0 + (my_r - my_c * TR);
+    const bool my_live = my_y < ny;
     const int kx_stride = 3 * nz * ny;                      // S elements between kx blocks
     const int row_off = (my_c * nz + z) * ny + my_y;        // (c, z, y) offset inside a kx block
-    // both rows in one aligned 16-byte copy when ny is even (then every pair offset is even)
-    const bool wide_copy = sizeof(cx<T>) == 8 && (ny & 1) == 0;
     {
-        cx<T>* dst = sm + 2 * (my_p * XH);
+        cx<T>* dst = sm + my_r * XHP;
         for (int k = my_k0; k < XH; k += KSTEP) {
-            const cx<T>* src = S + (k * kx_stride + row_off);
-            if (live1 && wide_copy) {
-                cp_async<16>(dst + 2 * k, src);
-            } else {
-                if (live0) cp_async<sizeof(cx<T>)>(dst + 2 * k, src);
-                else dst[2 * k] = cx<T>{0, 0};
-                if (live1) cp_async<sizeof(cx<T>)>(dst + 2 * k + 1, src + 1);
-                else dst[2 * k + 1] = cx<T>{0, 0};
-            }
+            if (my_live) cp_async<sizeof(cx<T>)>(dst + k, S + (k * kx_stride + row_off));
+            else dst[k] = cx<T>{0, 0};
         }
     }
     stage_twiddles<T, LOG2L>(tws, tw);
@@ -589,17 +576,21 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     const bool a_task = ta < P * N1;
     const int pa = ta / N1, n1 = ta % N1;
     if (a_task) {
-        const cx<T>* AB = sm + 2 * (pa * XH); // (A[k], B[k]) adjacent
+        const cx<T>* A = sm + (2 * pa) * XHP;
+        const cx<T>* B = A + XHP;
 #pragma unroll
         for (int m = 0; m < RA; ++m) {
             const int k = n1 + N1 * (LA * m + ha);
-            const int kk = 2 * k <= L ? k : L - k;
-            cx<T> a, b;
-            load_pair<T>(AB + 2 * kk, a, b);
             cx<T> zv;
-            if (k == 0 || 2 * k == L) zv = cx<T>{a.x, b.x};
-            else if (2 * k < L) zv = cx<T>{a.x - b.y, a.y + b.x};
-            else zv = cx<T>{a.x + b.y, b.x - a.y};
+            if (k == 0 || 2 * k == L) {
+                zv = cx<T>{A[k].x, B[k].x};
+            } else if (2 * k < L) {
+                const cx<T> a = A[k], b = B[k];
+                zv = cx<T>{a.x - b.y, a.y + b.x};
+            } else {
+                const cx<T> a = A[L - k], b = B[L - k];
+                zv = cx<T>{a.x + b.y, b.x - a.y};
+            }
             v[m] = zv;
         }
         if constexpr (LA == 2) dft_pair<RA, +1, RA>(v, ha);
@@ -757,22 +748,15 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
         }
     }
     __syncthreads();
-    // ---- 3c. separate the packed rows, write the next step's half spectra (kx-major): both
-    // rows of a pair from one Z row, stored side by side (one 16-byte store for f32)
+    // ---- 3c. separate the packed rows, write the next step's half spectra (kx-major)
     const T half = T(0.5);
-    if (live0) {
-        const cx<T>* zr = sm + my_p * ZP;
+    if (my_live) {
+        const cx<T>* zr = sm + (my_r >> 1) * ZP;
+        const bool odd = my_r & 1;
         for (int k = my_k0; k < XH; k += KSTEP) {
             const cx<T> zk = zr[k], zm = zr[(L - k) & (L - 1)];
-            const cx<T> ea{(zk.x + zm.x) * half, (zk.y - zm.y) * half};
-            const cx<T> eb{(zk.y + zm.y) * half, (zm.x - zk.x) * half};
-            cx<T>* dst = S + (k * kx_stride + row_off);
-            if (live1 && wide_copy) {
-                store_pair<T>(dst, ea, eb);
-            } else {
-                dst[0] = ea;
-                if (live1) dst[1] = eb;
-            }
+            S[k * kx_stride + row_off] = odd ? cx<T>{(zk.y + zm.y) * half, (zm.x - zk.x) * half}
+                                             : cx<T>{(zk.x + zm.x) * half, (zk.y - zm.y) * half};
         }
     }
 
