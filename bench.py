@@ -417,6 +417,15 @@ def run_b200(args, world, rank, local):
             "step": {"alg_bytes": b_alg, "achieved": b_alg / (ms_step * 1e-3) / 1e9,
                      "frac": b_alg / (ms_step * 1e-3) / 1e9 / peak},
             "kernels_ms": prof}
+    # The FFT and LLG kernels are bounded by instruction issue, not by HBM: the warp
+    # instructions ncu counted per launch against the issue limit of 4 per clock per SM (148 SMs
+    # at the SM clock sampled during the timed region), over this run's kernel time.
+    wi = ps.get(top, {}).get("warp_inst") if ps else None
+    if wi:
+        roof["issue"] = {"warp_inst": wi, "sm_mhz": clk.summary().get("sm_mhz") or 1965.0,
+                         "limit_us": wi / (148 * 4 * (clk.summary().get("sm_mhz") or 1965.0)),
+                         "frac": wi / (148 * 4 * (clk.summary().get("sm_mhz") or 1965.0)) / (prof[top] * 1e3),
+                         "source": "ncu smsp__inst_executed.sum per launch (profiles/ncu_summary.json)"}
 
     # ---- end to end through the public API with host buffers (pinned): per step
     # H2D of M, one step, D2H of M

@@ -68,10 +68,11 @@ void launch_tensor_octant(double* E, int nx, int ny, int nz, double delta, cudaS
 void launch_tensor_entries(const int* ijk, int n, double delta, double* out, cudaStream_t stream);
 // Per-axis real cosine / sine transform of the octant (wrapped-kernel spectrum), fp64.
 // in dims (d0 fastest, d1, d2); transforms axis `axis` from length n to L/2+1 (1 if L == 1).
+// [k0, k0 + nk) selects a range of the output frequencies (nk < 0: all L/2+1).
 void launch_axis_transform(const double* in, double* out, int d0, int d1, int d2, int axis,
                            int L, const double2* cs_table, int odd_mask_for_axis,
                            long long comp_stride_in, long long comp_stride_out,
-                           cudaStream_t stream);
+                           cudaStream_t stream, int k0 = 0, int nk = -1);
 void launch_cs_table(double2* cs, int L, cudaStream_t stream);
 template <typename T>
 void launch_tensor_finalize(const double* spec, T* out, long long count, double scale,

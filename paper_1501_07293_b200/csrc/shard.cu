@@ -222,15 +222,19 @@ public:
         const char* pe = std::getenv("MMB_SHARD_PEER");
         peer_ = pe && pe[0] == '1' && world > 1;
 
-        // tensor spectrum for all kx once (fast layout [kx][kz][ky][6]), sliced per rank
-        DevBuf<T> kfull;
-        build_full_tensor(kfull);
-
+        // the prism-sum octant once; each rank's tensor spectrum only for its columns
+        {
+            DevBuf<double> E;
+            build_octant(E);
+            if (emulated_) {
+                for (int r = 0; r < world; ++r) ranks_.push_back(make_rank(r, E));
+            } else {
+                ranks_.push_back(make_rank(my_rank, E));
+            }
+        }
         if (emulated_) {
-            for (int r = 0; r < world; ++r) ranks_.push_back(make_rank(r, kfull));
             transport_ = std::make_unique<LoopbackTransport>();
         } else {
-            ranks_.push_back(make_rank(my_rank, kfull));
             ncclUniqueId id;
             std::memcpy(&id, nccl_id, sizeof(id));
             nck(ncclCommInitRank(&comm_, world, id, my_rank), "ncclCommInitRank");
@@ -305,6 +309,7 @@ public:
     }
 
     void step(long long n) override {
+        NvtxRange r("mmb::sharded_step");
         for (long long i = 0; i < n; ++i) {
             prime();
             if (peer_) exchange_and_yz_peer(1, true);
@@ -604,6 +609,7 @@ private:
     // range of q's chunk-j columns (its planes of them) and receives each peer's planes of its
     // own chunk-j columns into that peer's receive block. Backward: the reverse.
     void exchange_chunk(int j, bool backward) {
+        NvtxRange r(backward ? "mmb::a2a_backward" : "mmb::a2a_forward");
         const long long ny = d_.ny;
         transport_->begin(comm_stream_);
         for (auto& rp : ranks_) {
@@ -826,12 +832,21 @@ private:
         }
     }
 
-    void build_full_tensor(DevBuf<T>& out) {
+    // The prism-sum octant (fp64, every offset) once; each rank's spectrum slice is built from
+    // it for that rank's kx columns only (the x pass evaluates just those frequencies, so the y
+    // and z passes and their fp64 temporaries shrink by the world size).
+    void build_octant(DevBuf<double>& E) {
+        E.alloc(6 * static_cast<size_t>(g_.n));
+        launch_tensor_octant(E.p, g_.nx, g_.ny, g_.nz, d_.delta, stream_);
+    }
+
+    void build_rank_tensor(const DevBuf<double>& E, int k0, int ncols, DevBuf<T>& out) {
         const Geom& g = g_;
+        const int nc = std::max(ncols, 1);
         const long long c0 = g.n;
-        const long long c1 = static_cast<long long>(g.xh) * g.ny * g.nz;
-        const long long c2 = static_cast<long long>(g.xh) * g.yh * g.nz;
-        const long long c3 = static_cast<long long>(g.xh) * g.yh * g.zh;
+        const long long c1 = static_cast<long long>(nc) * g.ny * g.nz;
+        const long long c2 = static_cast<long long>(nc) * g.yh * g.nz;
+        const long long c3 = static_cast<long long>(nc) * g.yh * g.zh;
         DevBuf<double2> csx, csy, csz;
         csx.alloc(g.lx);
         csy.alloc(g.ly);
@@ -839,26 +854,20 @@ private:
         launch_cs_table(csx.p, g.lx, stream_);
         launch_cs_table(csy.p, g.ly, stream_);
         launch_cs_table(csz.p, g.lz, stream_);
-        DevBuf<double> a3;
-        {
-            DevBuf<double> E, a1, a2;
-            E.alloc(6 * static_cast<size_t>(c0));
-            launch_tensor_octant(E.p, g.nx, g.ny, g.nz, d_.delta, stream_);
-            a1.alloc(6 * c1);
-            launch_axis_transform(E.p, a1.p, g.nx, g.ny, g.nz, 0, g.lx, csx.p, 0x06, c0, c1, stream_);
-            a2.alloc(6 * c2);
-            launch_axis_transform(a1.p, a2.p, g.xh, g.ny, g.nz, 1, g.ly, csy.p, 0x12, c1, c2, stream_);
-            a3.alloc(6 * c3);
-            launch_axis_transform(a2.p, a3.p, g.xh, g.yh, g.nz, 2, g.lz, csz.p, 0x14, c2, c3, stream_);
-            ck(cudaStreamSynchronize(stream_), "tensor sync");
-        }
+        DevBuf<double> a1, a2, a3;
+        a1.alloc(6 * c1);
+        launch_axis_transform(E.p, a1.p, g.nx, g.ny, g.nz, 0, g.lx, csx.p, 0x06, c0, c1, stream_, k0, nc);
+        a2.alloc(6 * c2);
+        launch_axis_transform(a1.p, a2.p, nc, g.ny, g.nz, 1, g.ly, csy.p, 0x12, c1, c2, stream_);
+        a3.alloc(6 * c3);
+        launch_axis_transform(a2.p, a3.p, nc, g.yh, g.nz, 2, g.lz, csz.p, 0x14, c2, c3, stream_);
         out.alloc(6 * c3);
-        launch_tensor_finalize_fast<T>(a3.p, out.p, g.xh, g.yh, g.zh,
+        launch_tensor_finalize_fast<T>(a3.p, out.p, nc, g.yh, g.zh,
                                        1.0 / (static_cast<double>(g.lx) * g.ly * g.lz), stream_);
         ck(cudaStreamSynchronize(stream_), "tensor sync");
     }
 
-    std::unique_ptr<Rank<T>> make_rank(int r, const DevBuf<T>& kfull) {
+    std::unique_ptr<Rank<T>> make_rank(int r, const DevBuf<double>& E) {
         auto R = std::make_unique<Rank<T>>();
         R->rank = r;
         R->z0 = slabs_[r].first;
@@ -890,11 +899,7 @@ private:
         }
         if (!peer_) R->recv.alloc(static_cast<size_t>(std::max(off, 1LL)));
         if (!yz_) R->s2.alloc(static_cast<size_t>(std::max(R->ncols, 1)) * 3 * d_.nz * g_.ly);
-        const size_t per_kx = static_cast<size_t>(g_.zh) * g_.yh * 6;
-        R->kspec.alloc(std::max(R->ncols, 1) * per_kx);
-        if (R->ncols > 0)
-            ck(cudaMemcpyAsync(R->kspec.p, kfull.p + R->k0 * per_kx, R->ncols * per_kx * sizeof(T),
-                               cudaMemcpyDeviceToDevice, stream_), "tensor slice");
+        build_rank_tensor(E, R->k0, R->ncols, R->kspec);
         R->twx.alloc(2 * g_.lx);
         R->twy.alloc(2 * g_.ly);
         R->twz.alloc(2 * g_.lz);
@@ -968,7 +973,16 @@ private:
     void sync_and_check() {
         ck(cudaStreamSynchronize(comm_stream_), "sync");
         ck(cudaStreamSynchronize(stream_), "sync");
+        check_comm();
         check_numerical();
+    }
+
+    // an asynchronous NCCL failure (a peer died, a network error) surfaces as a CUDA-class error
+    void check_comm() {
+        if (!comm_) return;
+        ncclResult_t st = ncclSuccess;
+        nck(ncclCommGetAsyncError(comm_, &st), "ncclCommGetAsyncError");
+        if (st != ncclSuccess) throw cuda_error(std::string("NCCL asynchronous error: ") + ncclGetErrorString(st));
     }
 
     mmb_desc d_;

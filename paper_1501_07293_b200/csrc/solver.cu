@@ -208,6 +208,7 @@ public:
     // consecutive steps per digit (at most q + 5 graph launches, so a short run replays at the
     // long-run rate); only the 1-step graph flips the ping-pong buffer
     void step(long long n) override {
+        NvtxRange r("mmb::step");
         if (n > 0) prime();
         for (; n >= (1LL << kMaxLog2Batch); n -= (1LL << kMaxLog2Batch)) launch_graph(kMaxLog2Batch);
         for (int b = kMaxLog2Batch - 1; b >= 0; --b)
@@ -279,6 +280,7 @@ public:
 
     long long run(long long steps, long long cadence, double stop_torque, mmb_record_fn fn,
                   void* user) override {
+        NvtxRange r("mmb::run");
         // Simulation<T>::run (llg.cpp:110-124): record on absolute step_ % cadence == 0, stop
         // when sqrt(last_torque_sq)/ms^2 < stop_torque.
         const double ms2 = d_.ms * d_.ms;

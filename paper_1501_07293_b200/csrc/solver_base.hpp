@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstddef>
 #include <memory>
@@ -19,6 +20,15 @@ struct numerical_error : std::runtime_error {
 };
 struct cuda_error : std::runtime_error {
     using std::runtime_error::runtime_error;
+};
+
+// NVTX range for the host-side phases (step launches, exchanges, queries): header-only NVTX
+// v3, visible to nsys / ncu range filters, no-ops when no tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 inline void ck(cudaError_t e, const char* what) {

@@ -37,7 +37,7 @@ __global__ void k_cs_table(double2* cs, int L) {
 __global__ void k_axis_transform(const double* __restrict__ in, double* __restrict__ out, int d0,
                                  int d1, int d2, int axis, int L, int nout,
                                  const double2* __restrict__ cs, int odd_mask, long long csi,
-                                 long long cso) {
+                                 long long cso, int k0) {
     const int c = blockIdx.y;
     const bool odd = (odd_mask >> c) & 1;
     int od[3] = {d0, d1, d2};
@@ -50,7 +50,7 @@ __global__ void k_axis_transform(const double* __restrict__ in, double* __restri
     idx[0] = static_cast<int>(f % od[0]);
     idx[1] = static_cast<int>((f / od[0]) % od[1]);
     idx[2] = static_cast<int>(f / (static_cast<long long>(od[0]) * od[1]));
-    const int k = idx[axis];
+    const int k = idx[axis] + k0; // output frequencies [k0, k0 + nout)
     long long stride_in = 1;
     if (axis >= 1) stride_in *= d0;
     if (axis >= 2) stride_in *= d1;
@@ -129,13 +129,13 @@ void launch_cs_table(double2* cs, int L, cudaStream_t stream) {
 
 void launch_axis_transform(const double* in, double* out, int d0, int d1, int d2, int axis, int L,
                            const double2* cs_table, int odd_mask, long long csi, long long cso,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, int k0, int nk) {
     int od[3] = {d0, d1, d2};
-    od[axis] = (L == 1) ? 1 : L / 2 + 1;
+    od[axis] = nk >= 0 ? nk : ((L == 1) ? 1 : L / 2 + 1);
     const long long total = static_cast<long long>(od[0]) * od[1] * od[2];
     const dim3 grid(static_cast<unsigned>((total + 255) / 256), 6);
     k_axis_transform<<<grid, 256, 0, stream>>>(in, out, d0, d1, d2, axis, L, od[axis], cs_table,
-                                               odd_mask, csi, cso);
+                                               odd_mask, csi, cso, k0);
     check_launch();
 }
 

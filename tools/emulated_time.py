@@ -21,8 +21,8 @@ a = ap.parse_args()
 nx, ny, nz, delta, a_ex, ms, hk, alpha, dt, prec = WORKLOADS[a.workload]
 spec = ProblemSpec(name=a.workload, grid=Grid(nx, ny, nz, delta), material=MaterialParams(a_ex, ms, hk, alpha), dt=dt)
 sim = make_emulated_sharded_simulation(spec, Precision.f32, a.world)
-sim.set_magnetization(random_state(nx, ny, nz, ms, np.float32))
+sim.set_magnetization(random_state(nx, ny, nz, ms, prec))
 sim.time_steps(2)
 t = sim.time_steps(a.steps) / a.steps
-print(f"{a.workload} world {a.world} peer={os.environ.get('MMB_SHARD_PEER', '0')}: {t:.3f} ms/step "
+print(f"{a.workload} world {a.world} peer={os.environ.get('MMB_SHARD_PEER', '0')} chunks={os.environ.get('MMB_SHARD_CHUNKS', '4')}: {t:.3f} ms/step "
       f"(all ranks on one GPU)")

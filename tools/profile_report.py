@@ -111,7 +111,9 @@ def main(tag, workload, rep, launch_csv=None):
     table = json.load(open(js)) if os.path.exists(js) else {}
     table[workload] = {d["kernel"]: {"dram_bytes": d.get("dram_read", 0) + d.get("dram_write", 0),
                                      "dram_read": d.get("dram_read"), "dram_write": d.get("dram_write"),
-                                     "time_us": d.get("time_us"), "capture": tag} for d in ks}
+                                     "time_us": d.get("time_us"), "warp_inst": d.get("warp_inst"),
+                                     "issue_pct": d.get("issue_pct"), "fma_pipe_pct": d.get("fma_pipe_pct"),
+                                     "capture": tag} for d in ks}
     json.dump(table, open(js, "w"), indent=1)
     print(open(path).read())
 
