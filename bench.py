@@ -445,13 +445,25 @@ def run_b200(args, world, rank, local):
         sim.get_m_into(pin_out)
     te = max_over_ranks(world, time.perf_counter() - t0)
     copy_ms = pcie_copy_ms(3 * n * w, dtype)
+    # a streaming run through the public API: M uploaded once, then mmb_run with a <m> record
+    # (device -> host, 24 bytes) after every step, delivered through the device record ring
+    from paper_1501_07293_b200 import RunOptions
+    recs = []
+    barrier(world)
+    t0 = time.perf_counter()
+    sim.set_m_from(pin_in)
+    sim.run(RunOptions(steps=args.steps, cadence=1, sink=recs.append))
+    tr = max_over_ranks(world, time.perf_counter() - t0)
     e2e = {"value": n * args.steps * world / te, "unit": UNIT,
            "h2d_bytes_per_step": 3 * n * w, "d2h_bytes_per_step": 3 * n * w,
            "api": "mmb_set_m + mmb_step(1) + mmb_get_m per step (libmmb.so C-ABI via ctypes)",
            "ms_per_step": 1e3 * te / args.steps,
            "pcie_floor_ms": copy_ms + ms_step,
            "note": "per step: pinned H2D of M, one graph-replayed step, pinned D2H of M (dependent, so the "
-                   "copies cannot overlap); pcie_floor_ms = device time of the same two copies + the step"}
+                   "copies cannot overlap); pcie_floor_ms = device time of the same two copies + the step",
+           "run_records": {"value": n * args.steps * world / tr, "unit": UNIT,
+                           "h2d_bytes": 3 * n * w, "d2h_bytes_per_step": 24, "records": len(recs),
+                           "api": "mmb_set_m once + mmb_run(steps, cadence 1, record callback)"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

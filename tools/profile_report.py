@@ -32,7 +32,9 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "
 def short_name(full):
     base = full.split("(")[0].split("::")[-1].split("<")[0].strip()
     if base.startswith("k_y<") or base == "k_y" or base == "k_yrow":
-        return "y_inv" if ", 1>" in full.split("(")[0] else "y_fwd"
+        targs = full.split("(")[0].split("<", 1)[-1].rstrip(">").split(",")
+        inv = len(targs) >= 3 and targs[2].strip() in ("1", "(int)1")
+        return "y_inv" if inv else "y_fwd"
     return SHORT.get(base, base)
 
 
