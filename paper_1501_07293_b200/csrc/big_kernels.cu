@@ -11,6 +11,7 @@
 // register four-step of fft4.cuh with unit-stride global loads/stores.
 #include <cstdio>
 #include <stdexcept>
+#include <type_traits>
 #include <string>
 
 #include "fast.hpp"
@@ -160,19 +161,23 @@ __global__ void __launch_bounds__(kZThreads)
 
     // load the nz live planes (async, coalesced over ky): each thread keeps its w and walks
     // the (c, z) planes with a fixed stride, carrying (c, z) instead of dividing
-    {
-        static_assert(kZThreads % W == 0, "pencil tile");
-        constexpr int CZSTEP = kZThreads / W;
-        const int w = tid % W;
-        int c = 0, z = tid / W;
+    // Whole tiles (Ly a multiple of W) move VEC consecutive ky per 16-byte copy.
+    auto load_tile = [&](auto vec) {
+        constexpr int VEC = decltype(vec)::value;
+        constexpr int TW = W / VEC; // threads per (c, z) row
+        static_assert(kZThreads % TW == 0, "pencil tile");
+        constexpr int CZSTEP = kZThreads / TW;
+        const int w = (tid % TW) * VEC;
+        int c = 0, z = tid / TW;
         while (z >= nz) {
             z -= nz;
             ++c;
         }
-        const cx<T>* src = blk + static_cast<long long>(tid / W) * zpitch + w;
-        for (int cz = tid / W; cz < 3 * nz; cz += CZSTEP) {
+        const cx<T>* src = blk + static_cast<long long>(tid / TW) * zpitch + w;
+        for (int cz = tid / TW; cz < 3 * nz; cz += CZSTEP) {
             cx<T>* d = A + (c * LZ + z) * W + w;
-            if (w < wl) cp_async<sizeof(cx<T>)>(d, src);
+            if (VEC > 1) cp_async<16>(d, src);
+            else if (w < wl) cp_async<sizeof(cx<T>)>(d, src);
             else *d = cx<T>{0, 0};
             src += CZSTEP * zpitch;
             z += CZSTEP;
@@ -181,7 +186,10 @@ __global__ void __launch_bounds__(kZThreads)
                 ++c;
             }
         }
-    }
+    };
+    constexpr int VEC16 = 16 / static_cast<int>(sizeof(cx<T>));
+    if (VEC16 > 1 && wl == W && (ly % VEC16) == 0) load_tile(std::integral_constant<int, VEC16>{});
+    else load_tile(std::integral_constant<int, 1>{});
     stage_twiddles<T, LOG2LZ>(tws, tw);
     cp_async_wait_all();
     __syncthreads();
