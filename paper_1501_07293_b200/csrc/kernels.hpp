@@ -59,6 +59,8 @@ template <typename T>
 void launch_energy(const T* m, const T* hd, const Geom& g, double ku_over_ms2,
                    const StepCtl* ctl, double* partial, double* out, cudaStream_t stream);
 int reduce_blocks(long long n);
+// keep `stream` busy for ns nanoseconds (timing helper: the host enqueues the timed work meanwhile)
+void launch_spin(unsigned long long ns, cudaStream_t stream);
 
 // ---- one-time tensor precompute (tensor_kernels.cu) ------------------------------------
 // K0: fp64 prism-sum entries on the non-negative octant, E[6][nz][ny][nx]

@@ -336,6 +336,22 @@ int llg_blocks(const Geom& g) {
     return ((g.nx + kTileX - 1) / kTileX) * ((g.ny + kTileY - 1) / kTileY) * g.nz;
 }
 
+// One thread spinning on the global timer: keeps the stream busy for `ns` nanoseconds so that
+// the host has enqueued a timed sequence before its start event is processed (the timing then
+// excludes host launch latency, as in a long run where the device runs ahead of the host).
+__global__ void k_spin(unsigned long long ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
+void launch_spin(unsigned long long ns, cudaStream_t stream) {
+    k_spin<<<1, 1, 0, stream>>>(ns);
+    check_launch();
+}
+
 void launch_torque_partials(const double* tpart, int nb, StepCtl* ctl, cudaStream_t stream) {
     k_torque_partials<<<1, 256, 0, stream>>>(tpart, nb, ctl);
     check_launch();

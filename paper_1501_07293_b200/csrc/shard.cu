@@ -380,6 +380,7 @@ public:
         ck(cudaEventCreate(&a), "event");
         ck(cudaEventCreate(&b), "event");
         prime();
+        launch_spin(200000ull, stream_); // the host enqueues the timed steps meanwhile
         ck(cudaEventRecord(a, stream_), "record");
         step(n);
         ck(cudaEventRecord(b, stream_), "record");

@@ -387,6 +387,9 @@ public:
         cudaEvent_t a, b;
         ck(cudaEventCreate(&a), "event");
         ck(cudaEventCreate(&b), "event");
+        // the stream is busy for 200 us before the start event, so every graph launch of the
+        // timed sequence is already queued when the device reaches it (device time only)
+        launch_spin(200000ull, stream_);
         ck(cudaEventRecord(a, stream_), "record");
         step(n);
         ck(cudaEventRecord(b, stream_), "record");
