@@ -89,6 +89,15 @@ void mmb_free(mmb_ctx* ctx);
 
 int mmb_set_m(mmb_ctx* ctx, const void* mx, const void* my, const void* mz);
 int mmb_get_m(mmb_ctx* ctx, void* mx, void* my, void* mz);
+/* Stream-ordered variants for pipelined host I/O (no reference counterpart): the copies go
+ * through device staging buffers on their own host->device / device->host streams, ordered
+ * with the steps enqueued around them, so a loop of set_m_async, mmb_step, get_m_async keeps
+ * both PCIe directions and the step in flight together. The host arrays must stay valid and
+ * unchanged (set) / untouched (get) until the next mmb_synchronize (or any synchronising
+ * call); get_m_async delivers the state at its position in the sequence. Sharded handles run
+ * them synchronously. */
+int mmb_set_m_async(mmb_ctx* ctx, const void* mx, const void* my, const void* mz);
+int mmb_get_m_async(mmb_ctx* ctx, void* mx, void* my, void* mz);
 
 int mmb_step(mmb_ctx* ctx, long long n);
 int mmb_step_index(const mmb_ctx* ctx, long long* out);

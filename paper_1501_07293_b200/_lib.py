@@ -19,7 +19,7 @@ EXPORTS = [
     "mmb_tensor_octant", "mmb_upload_tensor_octant", "mmb_time_steps", "mmb_profile_step",
     "mmb_launches_per_step", "mmb_device_bytes", "mmb_nccl_unique_id", "mmb_create_sharded",
     "mmb_create_emulated", "mmb_slab", "mmb_validate", "mmb_string_free", "mmb_path_info",
-    "mmb_random_unit_field",
+    "mmb_random_unit_field", "mmb_set_m_async", "mmb_get_m_async",
 ]
 
 
@@ -80,6 +80,8 @@ def load():
     L.mmb_free.restype = None
     L.mmb_set_m.argtypes = [vp, vp, vp, vp]
     L.mmb_get_m.argtypes = [vp, vp, vp, vp]
+    L.mmb_set_m_async.argtypes = [vp, vp, vp, vp]
+    L.mmb_get_m_async.argtypes = [vp, vp, vp, vp]
     L.mmb_step.argtypes = [vp, ll]
     L.mmb_step_index.argtypes = [vp, C.POINTER(ll)]
     L.mmb_average.argtypes = [vp, C.POINTER(d)]

@@ -179,6 +179,13 @@ public:
                 if (ge) cudaGraphExecDestroy(ge);
         if (ctl_host_) cudaFreeHost(ctl_host_);
         if (rec_host_) cudaFreeHost(rec_host_);
+        if (h2d_) {
+            cudaStreamSynchronize(h2d_);
+            cudaStreamSynchronize(d2h_);
+            for (cudaEvent_t e : {in_ready_, in_free_, out_ready_, out_free_}) cudaEventDestroy(e);
+            cudaStreamDestroy(h2d_);
+            cudaStreamDestroy(d2h_);
+        }
         if (stream_) cudaStreamDestroy(stream_);
     }
 
@@ -207,6 +214,48 @@ public:
     // n steps as graph replays: n = 32 q + binary digits of the rest, one graph of 2^b
     // consecutive steps per digit (at most q + 5 graph launches, so a short run replays at the
     // long-run rate); only the 1-step graph flips the ping-pong buffer
+    // Pipelined host I/O: host <-> staging copies on their own streams, staging <-> M on the
+    // main stream, events in both directions so a staging buffer is reused only after its
+    // previous copy finished.
+    void set_m_async(const void* x, const void* y, const void* z) override {
+        ensure_io();
+        const size_t n = g_.n;
+        const void* src[3] = {x, y, z};
+        if (in_free_rec_) ck(cudaStreamWaitEvent(h2d_, in_free_, 0), "wait");
+        for (int c = 0; c < 3; ++c)
+            ck(cudaMemcpyAsync(in_.p + c * n, src[c], n * sizeof(T), cudaMemcpyHostToDevice, h2d_), "set_m_async");
+        ck(cudaEventRecord(in_ready_, h2d_), "record");
+        ck(cudaStreamWaitEvent(stream_, in_ready_, 0), "wait");
+        ck(cudaMemcpyAsync(m_[cur_].p, in_.p, 3 * n * sizeof(T), cudaMemcpyDeviceToDevice, stream_), "set_m_async");
+        ck(cudaEventRecord(in_free_, stream_), "record");
+        in_free_rec_ = true;
+        s_valid_ = false;
+    }
+
+    void get_m_async(void* x, void* y, void* z) override {
+        ensure_io();
+        const size_t n = g_.n;
+        void* dst[3] = {x, y, z};
+        if (out_free_rec_) ck(cudaStreamWaitEvent(stream_, out_free_, 0), "wait");
+        ck(cudaMemcpyAsync(out_.p, m_[cur_].p, 3 * n * sizeof(T), cudaMemcpyDeviceToDevice, stream_), "get_m_async");
+        ck(cudaEventRecord(out_ready_, stream_), "record");
+        ck(cudaStreamWaitEvent(d2h_, out_ready_, 0), "wait");
+        for (int c = 0; c < 3; ++c)
+            ck(cudaMemcpyAsync(dst[c], out_.p + c * n, n * sizeof(T), cudaMemcpyDeviceToHost, d2h_), "get_m_async");
+        ck(cudaEventRecord(out_free_, d2h_), "record");
+        out_free_rec_ = true;
+    }
+
+    void ensure_io() {
+        if (h2d_) return;
+        ck(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking), "cudaStreamCreate");
+        for (cudaEvent_t* e : {&in_ready_, &in_free_, &out_ready_, &out_free_})
+            ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+        in_.alloc(3 * static_cast<size_t>(g_.n));
+        out_.alloc(3 * static_cast<size_t>(g_.n));
+    }
+
     void step(long long n) override {
         NvtxRange r("mmb::step");
         if (n > 0) prime();
@@ -671,6 +720,10 @@ private:
 
     void sync_and_check() {
         ck(cudaStreamSynchronize(stream_), "sync");
+        if (h2d_) {
+            ck(cudaStreamSynchronize(h2d_), "sync");
+            ck(cudaStreamSynchronize(d2h_), "sync");
+        }
         check_numerical();
     }
 
@@ -679,6 +732,11 @@ private:
     StageTable st_{};
     cudaStream_t stream_ = nullptr;
     DevBuf<T> m_[2], hd_, heff_;
+    // pipelined host I/O (set_m_async / get_m_async): copy streams, staging buffers, events
+    cudaStream_t h2d_ = nullptr, d2h_ = nullptr;
+    DevBuf<T> in_, out_;
+    cudaEvent_t in_ready_ = nullptr, in_free_ = nullptr, out_ready_ = nullptr, out_free_ = nullptr;
+    bool in_free_rec_ = false, out_free_rec_ = false;
     DevBuf<cx<T>> S_, S2_, twx_, twy_, twz_;
     DevBuf<T> kspec_;
     DevBuf<double> partial_, red_, tpart_, rec_;
@@ -803,6 +861,16 @@ int mmb_set_m(mmb_ctx* ctx, const void* x, const void* y, const void* z) {
 int mmb_get_m(mmb_ctx* ctx, void* x, void* y, void* z) {
     if (!ctx || !x || !y || !z) return bad("mmb_get_m");
     return guarded([&] { ctx->s->get_m(x, y, z); return MMB_OK; });
+}
+
+int mmb_set_m_async(mmb_ctx* ctx, const void* x, const void* y, const void* z) {
+    if (!ctx || !x || !y || !z) return bad("mmb_set_m_async");
+    return guarded([&] { ctx->s->set_m_async(x, y, z); return MMB_OK; });
+}
+
+int mmb_get_m_async(mmb_ctx* ctx, void* x, void* y, void* z) {
+    if (!ctx || !x || !y || !z) return bad("mmb_get_m_async");
+    return guarded([&] { ctx->s->get_m_async(x, y, z); return MMB_OK; });
 }
 
 int mmb_step(mmb_ctx* ctx, long long n) {

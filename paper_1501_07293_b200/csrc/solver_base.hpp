@@ -67,6 +67,9 @@ public:
     virtual int precision() const = 0;
     virtual void set_m(const void*, const void*, const void*) = 0;
     virtual void get_m(void*, void*, void*) = 0;
+    // stream-ordered host I/O (mmb_set_m_async / mmb_get_m_async); synchronous by default
+    virtual void set_m_async(const void* x, const void* y, const void* z) { set_m(x, y, z); }
+    virtual void get_m_async(void* x, void* y, void* z) { get_m(x, y, z); }
     virtual void step(long long n) = 0;
     virtual long long step_index() const = 0;
     virtual void average(double* out) = 0;

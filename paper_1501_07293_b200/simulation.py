@@ -182,6 +182,16 @@ class Simulation:
     def set_m_from(self, m: np.ndarray) -> None:
         _lib.check(self._L.mmb_set_m(self._h, _ptr(m[0]), _ptr(m[1]), _ptr(m[2])))
 
+    def set_m_async(self, m: np.ndarray) -> None:
+        """Stream-ordered upload from a caller-owned (ideally pinned) [3, nz, ny, nx] array that
+        must stay valid and unchanged until synchronize()."""
+        _lib.check(self._L.mmb_set_m_async(self._h, _ptr(m[0]), _ptr(m[1]), _ptr(m[2])))
+
+    def get_m_async(self, out: np.ndarray) -> None:
+        """Stream-ordered download of the state at this point of the sequence into a
+        caller-owned array, complete after synchronize()."""
+        _lib.check(self._L.mmb_get_m_async(self._h, _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
+
     # ---- parity hooks -----------------------------------------------------------------------
     def effective_field(self) -> np.ndarray:
         out = np.empty(self._shape(), dtype=self.dtype)
