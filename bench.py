@@ -86,14 +86,49 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region: an NVML
+    poller thread (~1 kHz) started right before and stopped right after it (the timed regions
+    are a few ms long, shorter than nvidia-smi's sampling period). Falls back to nvidia-smi
+    polling every 100 ms when NVML is unavailable."""
+
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index):
         self.index = index
+        self.samples = []
+        self.max_mhz = None
+        self.thread = None
+        self.stop = False
         self.proc = None
         self.path = None
 
+    def _poll(self, nv, h):
+        while not self.stop:
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:
+                pass
+            time.sleep(0.0005)
+
     def __enter__(self):
+        try:
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.nv = nv
+            self.thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self.thread.start()
+            while not self.samples:  # the poller is running before the timed region starts
+                time.sleep(0.0002)
+            return self
+        except Exception:
+            self.thread = None
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         try:
@@ -110,6 +145,9 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
+        if self.thread:
+            self.stop = True
+            self.thread.join(timeout=5)
         if self.proc:
             self.proc.terminate()
             try:
@@ -117,7 +155,25 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
+    def mark(self):
+        """Call right before and right after the timed call: the summary then covers the
+        samples between the two marks."""
+        self.marks = getattr(self, "marks", []) + [len(self.samples)]
+
     def summary(self):
+        if self.thread is not None or self.samples:
+            marks = getattr(self, "marks", [])
+            win = self.samples[marks[0]:marks[1]] if len(marks) >= 2 and marks[1] > marks[0] else self.samples
+            if not win:
+                return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+            sm = [s for s, _ in win]
+            bits = 0
+            for _, r in win:
+                bits |= r
+            reasons = sorted(n for n, c in self.NAMES if bits & getattr(self.nv, c, 0))
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                    "samples": len(sm), "sm_mhz_min": min(sm),
+                    "source": "NVML poller (~1 kHz) between the marks around the timed call"}
         rows = []
         try:
             for line in open(self.path):
@@ -325,12 +381,13 @@ def run_b200_sharded(args, world, rank, local):
     sim = make_sharded_simulation(spec, Precision.f32 if prec == "f32" else Precision.f64, rank, world,
                                   bytes(nid.cpu().numpy()), device=local)
     sim.set_magnetization(random_state(nx, ny, nz, ms, prec, z0=sim.z0, nz_local=sim.nz_local))
-    sim.time_steps(max(3, args.warmup))
     barrier(world)
     with ClockSampler(local) as clk:
         sim.time_steps(max(3, args.warmup))
         barrier(world)
+        clk.mark()
         t_ms = sim.time_steps(args.steps)
+        clk.mark()
     t_ms = max_over_ranks(world, t_ms)
     value = n * args.steps / (t_ms * 1e-3)
     ms_step = t_ms / args.steps
@@ -394,11 +451,12 @@ def run_b200(args, world, rank, local):
     # ---- device-resident throughput (value). The warm-up steps run right before the timed
     # ones (after the clock sampler started), so the SMs are at their load clock when the
     # timed region begins.
-    sim.time_steps(max(3, args.warmup))
     barrier(world)
     with ClockSampler(local) as clk:
         sim.time_steps(max(3, args.warmup))
+        clk.mark()
         t_ms = sim.time_steps(args.steps)
+        clk.mark()
     t_ms = max_over_ranks(world, t_ms)
     value = n * args.steps * world / (t_ms * 1e-3)
     ms_step = t_ms / args.steps
