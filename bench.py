@@ -73,6 +73,16 @@ def algorithmic_bytes(nx, ny, nz, w):
     k["y_fwd"] = half + padded
     k["z_mac"] = 2 * padded + tensor
     k["y_inv"] = padded + half
+    # SURVEY §8(d)'s canonical stage bytes of the stages each fused kernel implements (the
+    # north-star pipeline K1 x-fwd, K2 y-fwd, K3 z+MAC, K4 y-inv, K5 x-inv, K6 local terms)
+    if nz > 1:
+        k2 = half + padded
+        k3 = 2 * padded + tensor
+        k4 = padded + half
+    else:  # nz == 1: one fused y pass (forward, MAC, inverse) reads and writes the half spectrum
+        k2, k3, k4 = half, tensor, half
+    k["canonical"] = {"yz": k2 + k3 + k4, "xstep": k["x_inv"] + k["llg"] + k["x_fwd"],
+                      "y_fwd": k2, "z_mac": k3, "y_inv": k4}
     return canonical, k
 
 
@@ -475,6 +485,12 @@ def run_b200(args, world, rank, local):
             "step": {"alg_bytes": b_alg, "achieved": b_alg / (ms_step * 1e-3) / 1e9,
                      "frac": b_alg / (ms_step * 1e-3) / 1e9 / peak},
             "kernels_ms": prof}
+    # the same kernel credited with SURVEY §8(d)'s canonical bytes of the stages it fuses (the
+    # bytes the north-star stage pipeline moves for them; the fused kernel moves `alg_bytes`)
+    cb = kbytes.get("canonical", {}).get(top)
+    if cb:
+        roof["canonical_stages"] = {"alg_bytes": cb, "achieved": cb / (prof[top] * 1e-3) / 1e9,
+                                    "frac": cb / (prof[top] * 1e-3) / 1e9 / peak}
     # The FFT and LLG kernels are bounded by instruction issue, not by HBM: the warp
     # instructions ncu counted per launch against the issue limit of 4 per clock per SM (148 SMs
     # at the SM clock sampled during the timed region), over this run's kernel time.

@@ -29,3 +29,12 @@ def test_reference_arm_reports_unavailable_for_the_sharded_config():
     assert r.returncode == 0, r.stderr
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and "181 GB" in line["unavailable"]
+
+
+def test_canonical_stage_split_sums_to_the_step():
+    # the fused kernels' canonical stage bytes (roofline.canonical_stages) partition B_alg
+    for g in [(512, 512, 8), (256, 256, 1), (128, 32, 1), (1024, 1024, 32), (2048, 2048, 64)]:
+        b, k = bench.algorithmic_bytes(*g, 4)
+        c = k["canonical"]
+        assert c["yz"] + c["xstep"] == b
+        assert c["y_fwd"] + c["z_mac"] + c["y_inv"] == c["yz"]
