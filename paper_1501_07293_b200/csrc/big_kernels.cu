@@ -130,8 +130,14 @@ __global__ void __launch_bounds__(YR<LOG2L>::NT)
 // z pencils: W consecutive ky of one kx, all three components, Lz = 2^LOG2LZ >= 2 nz - 1.
 // pencils per CTA: 32 (f32) keeps the tile at 98 KB (two CTAs per SM) up to Lz = 64; the
 // Lz = 128 and 256 tiles halve / quarter it for the same occupancy
+#ifndef MMB_ZW_SHIFT8
+#define MMB_ZW_SHIFT8 1 // pencils per CTA at Lz = 256: 32 >> 1 = 16 (f32)
+#endif
+#ifndef MMB_ZW_SHIFT7
+#define MMB_ZW_SHIFT7 1 // pencils per CTA at Lz = 128: 32 >> 1 = 16 (f32)
+#endif
 template <typename T, int LOG2LZ>
-constexpr int zw() { return (sizeof(T) == 4 ? 32 : 16) >> (LOG2LZ >= 8 ? 2 : (LOG2LZ >= 7 ? 1 : 0)); }
+constexpr int zw() { return (sizeof(T) == 4 ? 32 : 16) >> (LOG2LZ >= 8 ? MMB_ZW_SHIFT8 : (LOG2LZ >= 7 ? MMB_ZW_SHIFT7 : 0)); }
 constexpr int kZThreads = 256;
 template <typename T, int LOG2LZ>
 constexpr int z_smem_bytes() {
