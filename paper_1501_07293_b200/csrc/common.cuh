@@ -13,6 +13,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace mmb {
@@ -22,6 +23,42 @@ template <> struct V2<float> { using type = float2; };
 template <> struct V2<double> { using type = double2; };
 template <typename T> using cx = typename V2<T>::type;
 
+// ---- packed fp32 pairs (sm_100a FADD2 / FMUL2 / FFMA2): one instruction for both halves of a
+// float2, each half rounded exactly as the scalar operation. ptxas folds the swaps, negations
+// and scalar broadcasts below into operand modifiers, so a complex add is one instruction and
+// a complex product two.
+__device__ __forceinline__ unsigned long long f2_bits(float2 a) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 f2_val(unsigned long long v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_val(r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_val(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_val(r);
+}
+// a * b + c per half, fused (one rounding)
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+    return f2_val(r);
+}
+
 template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return {a.x + b.x, a.y + b.y}; }
 template <typename C> __device__ __forceinline__ C csub(C a, C b) { return {a.x - b.x, a.y - b.y}; }
 template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
@@ -30,6 +67,33 @@ template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
 // a * conj(b)
 template <typename C> __device__ __forceinline__ C cmulc(C a, C b) {
     return {a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y};
+}
+// Register complex type of the kernels that use packed arithmetic (chosen per kernel: it pays
+// in the fused y/z and x-step kernels up to L = 1024, not in the lane-pair DFT_64 and
+// streaming kernels). Same layout as float2, converts both ways.
+struct __align__(8) pf2 {
+    float x, y;
+    pf2() = default;
+    __device__ __forceinline__ constexpr pf2(float a, float b) : x(a), y(b) {}
+    __device__ __forceinline__ pf2(float2 v) : x(v.x), y(v.y) {}
+    __device__ __forceinline__ operator float2() const { return make_float2(x, y); }
+};
+template <typename C> struct is_packed { static constexpr bool value = false; };
+template <> struct is_packed<pf2> { static constexpr bool value = true; };
+// the register complex type of a kernel on T at transform length 2^LOG2L
+template <typename T, int LOG2L>
+using rcx = typename std::conditional<(sizeof(T) == 4 && LOG2L <= 10), pf2, cx<T>>::type;
+
+__device__ __forceinline__ pf2 fma2(pf2 a, pf2 b, pf2 c) { return fma2(float2(a), float2(b), float2(c)); }
+// packed: (a.x b.x - a.y b.y, a.x b.y + a.y b.x) = a.x (b.x, b.y) + a.y (-b.y, b.x)
+template <> __device__ __forceinline__ pf2 cadd(pf2 a, pf2 b) { return add2(a, b); }
+template <> __device__ __forceinline__ pf2 csub(pf2 a, pf2 b) { return sub2(a, b); }
+template <> __device__ __forceinline__ pf2 cmul(pf2 a, pf2 b) {
+    return fma2(make_float2(a.y, a.y), make_float2(-b.y, b.x), mul2(make_float2(a.x, a.x), b));
+}
+// (a.x b.x + a.y b.y, a.y b.x - a.x b.y) = a.x (b.x, -b.y) + a.y (b.y, b.x)
+template <> __device__ __forceinline__ pf2 cmulc(pf2 a, pf2 b) {
+    return fma2(make_float2(a.y, a.y), make_float2(b.y, b.x), mul2(make_float2(a.x, a.x), make_float2(b.x, -b.y)));
 }
 template <typename C> __device__ __forceinline__ C czero() { return {0, 0}; }
 
@@ -101,7 +165,8 @@ __device__ __forceinline__ C rot64(C x) {
         constexpr double c = (M < 16) ? kCos64[M] : -kCos64[32 - M];
         constexpr double s0 = (M < 16) ? kCos64[16 - M] : kCos64[M - 16];
         const T cc = T(c), ss = T(SIGN * s0);
-        return C{x.x * cc - x.y * ss, x.x * ss + x.y * cc};
+        if constexpr (is_packed<C>::value) return cmul(x, C{cc, ss});
+        else return C{x.x * cc - x.y * ss, x.x * ss + x.y * cc};
     }
 }
 

@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
     constexpr int RP = fpitch<LOG2L>();
     constexpr int NT = yz_threads<T, LOG2L>();
     constexpr int RB = NT / N2; // rows per batch
+    using RC = rcx<T, LOG2L>; // register complex type (packed FFMA2 arithmetic for f32)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
 
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
     // ---- y forward, batches of RB rows
     for (int rb0 = 0; rb0 < rows; rb0 += RB) {
         const int nb = min(RB, rows - rb0);
-        cx<T> v[N2];
+        RC v[N2];
         const int ra = rb0 + tid / N1, n1 = tid % N1;
         const bool a_task = tid < nb * N1;
         if (a_task) {
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
 #pragma unroll
             for (int n2 = 0; n2 < NZ; ++n2) {
                 const int y = n1 + N1 * n2;
-                v[n2] = y < ny ? src[y] : cx<T>{0, 0};
+                v[n2] = y < ny ? RC(src[y]) : RC{0, 0};
             }
             DftP<N2, -1, NZ, N2>::run(v);
         }
@@ -309,15 +310,15 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
             cx<T>* dst = sm + ra * RP;
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) {
-                cx<T> w = v[k2];
-                if (k2 > 0) w = cmul(w, tws[k2 * N1 + n1]);
+                RC w = v[k2];
+                if (k2 > 0) w = cmul(w, RC(tws[k2 * N1 + n1]));
                 dst[fpad<LOG2L>(k2 * N1 + n1)] = w;
             }
         }
         __syncthreads();
         const int rbr = rb0 + tid / N2, k2 = tid % N2;
         const bool b_task = tid < nb * N2;
-        cx<T> u[N1];
+        RC u[N1];
         if (b_task) {
             const cx<T>* src = sm + rbr * RP;
 #pragma unroll
@@ -345,14 +346,14 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
             cx<T>* base = sm + (kxl * 3 * nz) * RP + fpad<LOG2L>(ky);
             if constexpr (ZM == 0) {
                 // nz == 1: MAC only
-                cx<T> a = base[0], b = base[RP], cc = base[2 * RP];
+                RC a = base[0], b = base[RP], cc = base[2 * RP];
                 T k6[6];
                 load6<T>(kb, k6);
                 if (fy) {
                     k6[1] = -k6[1];
                     k6[4] = -k6[4];
                 }
-                mac3<T>(k6, a, b, cc);
+                mac3(k6, a, b, cc);
                 base[0] = a;
                 base[RP] = b;
                 base[2 * RP] = cc;
@@ -364,12 +365,12 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
 #pragma unroll
                 for (int kzo = 0; kzo <= 8; ++kzo) load6<T>(kb + kzo * yh * 6, kk[kzo]);
 #endif
-                cx<T> w[3][16];
+                RC w[3][16];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
 #pragma unroll
                     for (int zz = 0; zz < 8; ++zz)
-                        w[c][zz] = zz < nz ? base[(c * nz + zz) * RP] : cx<T>{0, 0};
+                        w[c][zz] = zz < nz ? RC(base[(c * nz + zz) * RP]) : RC{0, 0};
                     DftP<16, -1, 8, 16>::run(w[c]);
                 }
 #pragma unroll
@@ -385,12 +386,12 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
                         k6[1] = -k6[1];
                         k6[4] = -k6[4];
                     }
-                    mac3<T>(k6, w[0][kzo], w[1][kzo], w[2][kzo]);
+                    mac3(k6, w[0][kzo], w[1][kzo], w[2][kzo]);
                     if (kzo != 0 && kzo != 8) {
                         // kz = 16 - kzo: xz and yz are odd in z
                         k6[2] = -k6[2];
                         k6[4] = -k6[4];
-                        mac3<T>(k6, w[0][16 - kzo], w[1][16 - kzo], w[2][16 - kzo]);
+                        mac3(k6, w[0][16 - kzo], w[1][16 - kzo], w[2][16 - kzo]);
                     }
                 }
 #pragma unroll
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
     // ---- y inverse, batches of RB rows, ny live outputs straight to HBM
     for (int rb0 = 0; rb0 < rows; rb0 += RB) {
         const int nb = min(RB, rows - rb0);
-        cx<T> v[N2];
+        RC v[N2];
         const int ra = rb0 + tid / N1, n1 = tid % N1;
         const bool a_task = tid < nb * N1;
         if (a_task) {
@@ -422,15 +423,15 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
             cx<T>* dst = sm + ra * RP;
 #pragma unroll
             for (int k2 = 0; k2 < N2; ++k2) {
-                cx<T> w = v[k2];
-                if (k2 > 0) w = cmulc(w, tws[k2 * N1 + n1]);
+                RC w = v[k2];
+                if (k2 > 0) w = cmulc(w, RC(tws[k2 * N1 + n1]));
                 dst[fpad<LOG2L>(k2 * N1 + n1)] = w;
             }
         }
         __syncthreads();
         const int rbr = rb0 + tid / N2, k2 = tid % N2;
         if (tid < nb * N2) {
-            cx<T> u[N1];
+            RC u[N1];
             const cx<T>* src = sm + rbr * RP;
 #pragma unroll
             for (int q = 0; q < N1; ++q) u[q] = src[fpad<LOG2L>(k2 * N1 + q)];
@@ -521,6 +522,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     using X = XS<LOG2L, PB, sizeof(T)>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = X::P, TR = X::TR, NT = X::NT;
     constexpr int XH = L / 2 + 1, XHP = X::XHP, EX = X::EX, ZP = X::ZP;
+    using RC = rcx<T, LOG2L>; // register complex type (packed FFMA2 arithmetic for f32, L <= 1024)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
     T* hm = reinterpret_cast<T*>(smem_raw); // [3*TR][nx] tile: H_demag, then M_{t+1}
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     // ---- 1b. inverse stage A on Z = A + iB (rows 2p, 2p+1 of the same component); lane
     // h of a pair task takes n2 = LA m + h
     constexpr int LA = X::LA, LB = X::LB, RA = N2 / LA, RBq = N1 / LB;
-    cx<T> v[RA];
+    RC v[RA];
     const int ha = LA == 2 ? pair_half(tid) : 0, ta = LA == 2 ? pair_task(tid) : tid;
     const bool a_task = ta < P * N1;
     const int pa = ta / N1, n1 = ta % N1;
@@ -602,8 +604,8 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
 #pragma unroll
         for (int kk = 0; kk < RA; ++kk) {
             const int k2 = kk + RA * ha;
-            cx<T> w = v[kk];
-            if (k2 > 0) w = cmulc(w, tws[k2 * N1 + n1]);
+            RC w = v[kk];
+            if (k2 > 0) w = cmulc(w, RC(tws[k2 * N1 + n1]));
             ex[k2 * EX] = w;
         }
     }
@@ -618,7 +620,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
         const int tb = tb0 + rnd * NT;
         const bool b_task = X::TM == 1 || tb < P * N2 * LB;
         const int pb = tb / N2, k2b = tb % N2;
-        cx<T> u[RBq];
+        RC u[RBq];
         constexpr int NO = N1 == 1 ? 1 : N1 / 2;
         if (b_task) {
             const cx<T>* ex = sm + (pb * N2 + k2b) * EX + hb_;
@@ -709,7 +711,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
         for (int m = 0; m < NZ; ++m) {
             const int x = n1 + N1 * (LA * m + ha);
             const bool in = x < nx;
-            v[m] = cx<T>{(in && va) ? tra[x] : T(0), (in && vb) ? trb[x] : T(0)};
+            v[m] = RC{(in && va) ? tra[x] : T(0), (in && vb) ? trb[x] : T(0)};
         }
         if constexpr (LA == 2) dft_pair<RA, -1, NZ>(v, ha);
         else DftP<N2, -1, NZ, N2>::run(v);
@@ -720,8 +722,8 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
 #pragma unroll
         for (int kk = 0; kk < RA; ++kk) {
             const int k2 = kk + RA * ha;
-            cx<T> w = v[kk];
-            if (k2 > 0) w = cmul(w, tws[k2 * N1 + n1]);
+            RC w = v[kk];
+            if (k2 > 0) w = cmul(w, RC(tws[k2 * N1 + n1]));
             ex[k2 * EX] = w;
         }
     }
@@ -732,7 +734,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
         const int tb = tb0 + rnd * NT;
         const bool b_task = X::TM == 1 || tb < P * N2 * LB;
         const int pb = tb / N2, k2b = tb % N2;
-        cx<T> u[RBq];
+        RC u[RBq];
         if (b_task) {
             const cx<T>* ex = sm + (pb * N2 + k2b) * EX + hb_;
 #pragma unroll

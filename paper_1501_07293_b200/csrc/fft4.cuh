@@ -77,17 +77,34 @@ struct DftP {
                 constexpr bool tan_form = (c < 0 ? -c : c) >= (sn < 0 ? -sn : sn);
                 C u;
                 T a;
-                if constexpr (tan_form) {
-                    const T rr = T(sn / c);
-                    a = T(c);
-                    u = C{fmaf_t(-rr, o[K].y, o[K].x), fmaf_t(rr, o[K].x, o[K].y)};
+                if constexpr (is_packed<C>::value) {
+                    // packed: 3 FFMA2 per butterfly (operand swaps, negations and the scalar
+                    // broadcasts fold into FFMA2 modifiers)
+                    const C oo = o[K], osw = C{oo.y, oo.x};
+                    if constexpr (tan_form) {
+                        const T rr = T(sn / c);
+                        a = T(c);
+                        u = fma2(C{-rr, rr}, osw, oo);
+                    } else {
+                        const T rr = T(c / sn);
+                        a = T(sn);
+                        u = fma2(C{rr, rr}, oo, C{-oo.y, oo.x});
+                    }
+                    v[K] = fma2(C{a, a}, u, e[K]);
+                    if constexpr (K + H < NO) v[K + H] = fma2(C{-a, -a}, u, e[K]);
                 } else {
-                    const T rr = T(c / sn);
-                    a = T(sn);
-                    u = C{fmaf_t(rr, o[K].x, -o[K].y), fmaf_t(rr, o[K].y, o[K].x)};
+                    if constexpr (tan_form) {
+                        const T rr = T(sn / c);
+                        a = T(c);
+                        u = C{fmaf_t(-rr, o[K].y, o[K].x), fmaf_t(rr, o[K].x, o[K].y)};
+                    } else {
+                        const T rr = T(c / sn);
+                        a = T(sn);
+                        u = C{fmaf_t(rr, o[K].x, -o[K].y), fmaf_t(rr, o[K].y, o[K].x)};
+                    }
+                    v[K] = C{fmaf_t(a, u.x, e[K].x), fmaf_t(a, u.y, e[K].y)};
+                    if constexpr (K + H < NO) v[K + H] = C{fmaf_t(-a, u.x, e[K].x), fmaf_t(-a, u.y, e[K].y)};
                 }
-                v[K] = C{fmaf_t(a, u.x, e[K].x), fmaf_t(a, u.y, e[K].y)};
-                if constexpr (K + H < NO) v[K + H] = C{fmaf_t(-a, u.x, e[K].x), fmaf_t(-a, u.y, e[K].y)};
             }
             combine<K + 1>(v, e, o);
         }
@@ -110,7 +127,8 @@ struct PairCombine {
             const C mine = h ? t : v[K];
             const T rx = __shfl_xor_sync(0xffffffffu, mine.x, XM);
             const T ry = __shfl_xor_sync(0xffffffffu, mine.y, XM);
-            v[K] = C{fmaf_t(sg, mine.x, rx), fmaf_t(sg, mine.y, ry)};
+            if constexpr (is_packed<C>::value) v[K] = fma2(C{sg, sg}, mine, C{rx, ry});
+            else v[K] = C{fmaf_t(sg, mine.x, rx), fmaf_t(sg, mine.y, ry)};
             PairCombine<R, SIGN, XM, K + 1>::run(v, h, sg);
         }
     }

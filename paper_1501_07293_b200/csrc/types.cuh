@@ -99,6 +99,14 @@ struct TensorSpec {
 
 // H^ = K M^ with the symmetric real tensor (rows {xx,xy,xz},{xy,yy,yz},{xz,yz,zz},
 // proj/src/demag.cpp:94-98).
+// packed registers: 9 FMUL2/FFMA2 instead of 18
+__device__ __forceinline__ void mac3(const float (&k)[6], pf2& a, pf2& b, pf2& c) {
+    const float2 mx = a, my = b, mz = c;
+    const auto bc = [](float v) { return make_float2(v, v); };
+    a = fma2(bc(k[2]), mz, fma2(bc(k[1]), my, mul2(bc(k[0]), mx)));
+    b = fma2(bc(k[4]), mz, fma2(bc(k[3]), my, mul2(bc(k[1]), mx)));
+    c = fma2(bc(k[5]), mz, fma2(bc(k[4]), my, mul2(bc(k[2]), mx)));
+}
 template <typename T>
 __device__ __forceinline__ void mac3(const T (&k)[6], cx<T>& a, cx<T>& b, cx<T>& c) {
     const cx<T> mx = a, my = b, mz = c;
