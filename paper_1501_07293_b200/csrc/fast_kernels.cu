@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
+#include <type_traits>
 #include <string>
 
 #include "fast.hpp"
@@ -447,6 +448,10 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
     }
 }
 
+#ifndef MMB_XS_PAIR_LLG
+#define MMB_XS_PAIR_LLG 1 // f32 local terms on packed cell pairs (even nx)
+#endif
+
 // ------------------------------------------------------------------ KXS: x^-1, LLG, x (fused)
 // One CTA per (TR consecutive y rows, one z plane), all three components:
 //   1. x-c2r of the convolved half spectra S -> H_demag tile (shared memory only),
@@ -654,6 +659,72 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     // 32-bit element indices (3 cs < 2^31) off one base: one 64-bit address per load instead
     // of 64-bit index arithmetic
     const int csi = static_cast<int>(cs);
+#if MMB_XS_PAIR_LLG
+    if constexpr (std::is_same_v<T, float>) {
+        if ((nx & 1) == 0) {
+            // f32, even nx: cell pairs (i, i+1) per thread on packed FP32 (CellPairLLG, bitwise
+            // CellLLG per cell). Every pair offset is even, so the centre, +-y and +-z loads,
+            // the H_demag reads and the stores are 8-byte vectors; the outer x neighbours are
+            // scalar loads from the same sectors. A missing neighbour is the cell's own centre
+            // (adds +0 to the exchange sum).
+            CellPairLLG pl;
+            pl.load(ctl, coeff, kan);
+            const int nxh = nx >> 1;
+            int yl = 0, ip = tid;
+            while (ip >= nxh) {
+                ip -= nxh;
+                ++yl;
+            }
+            for (; yl < TR; ) {
+                const int j = y0 + yl;
+                if (j >= ny) break;
+                const int i = 2 * ip;
+                const int f = z * sz + j * sy + i;
+                const bool xl = i > 0, xr = i + 2 < nx, ym = j > 0, yp = j + 1 < ny, zm = zg > 0,
+                           zp = zg + 1 < nzg;
+                float2 mc[3], ex[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int q = c * csi + f;
+                    const float2 ctr = __ldg(reinterpret_cast<const float2*>(m + q));
+                    float2 nb[6];
+                    nb[0] = make_float2(xl ? __ldg(m + (q - 1)) : ctr.x, ctr.x);
+                    nb[1] = make_float2(ctr.y, xr ? __ldg(m + (q + 2)) : ctr.y);
+                    nb[2] = ym ? __ldg(reinterpret_cast<const float2*>(m + (q - sy))) : ctr;
+                    nb[3] = yp ? __ldg(reinterpret_cast<const float2*>(m + (q + sy))) : ctr;
+                    nb[4] = zm ? __ldg(reinterpret_cast<const float2*>(m + (q - sz))) : ctr;
+                    nb[5] = zp ? __ldg(reinterpret_cast<const float2*>(m + (q + sz))) : ctr;
+                    mc[c] = ctr;
+                    ex[c] = CellPairLLG::exch(ctr, nb);
+                }
+                float2* hp = reinterpret_cast<float2*>(hm + yl * nx + i);
+                const int hc = (TR * nx) >> 1; // float2 stride between the component tiles
+                float2 hx = hp[0], hy = hp[hc], hz = hp[2 * hc];
+                pl.heff(mc[0], hx, hy, hz, ex[0], ex[1], ex[2]);
+                double t0, t1;
+                bool z0b, z1b;
+                pl.update(mc[0], mc[1], mc[2], hx, hy, hz, t0, t1, z0b, z1b);
+                tmax = fmax(tmax, fmax(t0, t1));
+                if (z0b || z1b)
+                    atomicMin(&ctl->bad_key, (static_cast<unsigned long long>(cur_step) << 36) |
+                                                 static_cast<unsigned long long>(
+                                                     f + (z0b ? 0 : 1) + static_cast<long long>(g.z0) * sz));
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    *reinterpret_cast<float2*>(mout + (c * csi + f)) = mc[c];
+                    hp[c * hc] = mc[c];
+                }
+                ip += NT;
+                while (ip >= nxh) {
+                    ip -= nxh;
+                    ++yl;
+                }
+            }
+            goto llg_done;
+        }
+    }
+#endif
+    {
     // walk the tile's cells with a fixed stride, carrying (yl, i) instead of dividing
     int yl = 0, i = tid;
     while (i >= nx) {
@@ -697,6 +768,10 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
             ++yl;
         }
     }
+    }
+#if MMB_XS_PAIR_LLG
+llg_done:
+#endif
     __syncthreads();
 
     // ---- 3a. forward stage A on the new tile (rows 2p, 2p+1 of one component)

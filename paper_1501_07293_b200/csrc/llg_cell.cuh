@@ -102,4 +102,73 @@ struct CellLLG {
     }
 };
 
+// Two horizontally adjacent cells (i, i+1) of f32 at once on packed FP32 pairs (sm_100a
+// FADD2/FMUL2, each half rounded as the scalar __fadd_rn/__fmul_rn): the same operations in
+// the same order as CellLLG, so each cell's H_eff and update are bitwise CellLLG's. Lane .x is
+// cell i, lane .y cell i+1. sqrt, the renormalising division and the fp64 torque stay
+// scalar per cell.
+struct CellPairLLG {
+    float2 coeff, kan, ax, ay, az, p1, p2;
+    float ms;
+
+    __device__ __forceinline__ void load(const StepCtl* ctl, float exch_coeff, float aniso_coeff) {
+        const auto bc = [](float v) { return make_float2(v, v); };
+        coeff = bc(exch_coeff);
+        kan = bc(aniso_coeff);
+        ax = bc(static_cast<float>(ctl->field[0]));
+        ay = bc(static_cast<float>(ctl->field[1]));
+        az = bc(static_cast<float>(ctl->field[2]));
+        p1 = bc(static_cast<float>(ctl->p1));
+        p2 = bc(static_cast<float>(ctl->p2));
+        ms = static_cast<float>(ctl->ms);
+    }
+
+    // sum over the six neighbours of (nbr - center) in the reference's order; a missing
+    // neighbour is passed as the center itself, which adds (center - center) = +0 and leaves
+    // the sum unchanged (a sum that starts at +0 is never -0 under round-to-nearest)
+    static __device__ __forceinline__ float2 exch(float2 ctr, const float2 (&nb)[6]) {
+        float2 sum = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) sum = add2(sum, sub2(nb[q], ctr));
+        return sum;
+    }
+
+    __device__ __forceinline__ void heff(float2 mx, float2& hx, float2& hy, float2& hz, float2 ex, float2 ey,
+                                         float2 ez) const {
+        hx = add2(hx, mul2(coeff, ex));
+        hy = add2(hy, mul2(coeff, ey));
+        hz = add2(hz, mul2(coeff, ez));
+        hx = add2(hx, mul2(kan, mx));
+        hx = add2(hx, ax);
+        hy = add2(hy, ay);
+        hz = add2(hz, az);
+    }
+
+    __device__ __forceinline__ void update(float2& mx, float2& my, float2& mz, float2 hx, float2 hy, float2 hz,
+                                           double& tsq0, double& tsq1, bool& zero0, bool& zero1) const {
+        const float2 tx = sub2(mul2(my, hz), mul2(mz, hy));
+        const float2 ty = sub2(mul2(mz, hx), mul2(mx, hz));
+        const float2 tz = sub2(mul2(mx, hy), mul2(my, hx));
+        const float2 dx = add2(mul2(p1, tx), mul2(p2, sub2(mul2(my, tz), mul2(mz, ty))));
+        const float2 dy = add2(mul2(p1, ty), mul2(p2, sub2(mul2(mz, tx), mul2(mx, tz))));
+        const float2 dz = add2(mul2(p1, tz), mul2(p2, sub2(mul2(mx, ty), mul2(my, tx))));
+        tsq0 = __dadd_rn(__dadd_rn(__dmul_rn(double(tx.x), double(tx.x)), __dmul_rn(double(ty.x), double(ty.x))),
+                         __dmul_rn(double(tz.x), double(tz.x)));
+        tsq1 = __dadd_rn(__dadd_rn(__dmul_rn(double(tx.y), double(tx.y)), __dmul_rn(double(ty.y), double(ty.y))),
+                         __dmul_rn(double(tz.y), double(tz.y)));
+        mx = add2(mx, dx);
+        my = add2(my, dy);
+        mz = add2(mz, dz);
+        const float2 s2 = add2(add2(mul2(mx, mx), mul2(my, my)), mul2(mz, mz));
+        const float mag0 = __fsqrt_rn(s2.x), mag1 = __fsqrt_rn(s2.y);
+        zero0 = mag0 == 0.f;
+        zero1 = mag1 == 0.f;
+        // an exactly zero magnitude leaves the cell unscaled, as the reference does
+        const float2 scale = make_float2(zero0 ? 1.f : __fdiv_rn(ms, mag0), zero1 ? 1.f : __fdiv_rn(ms, mag1));
+        mx = mul2(mx, scale);
+        my = mul2(my, scale);
+        mz = mul2(mz, scale);
+    }
+};
+
 } // namespace mmb
