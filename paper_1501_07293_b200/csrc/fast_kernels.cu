@@ -686,14 +686,17 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     const int q = c * csi + f;
-                    const float2 ctr = __ldg(reinterpret_cast<const float2*>(m + q));
+                    // a missing neighbour loads the centre's own address: every load is
+                    // unconditional and independent of the centre load (no select chain)
+                    const auto ld2 = [&](int o) { return __ldg(reinterpret_cast<const float2*>(m + o)); };
+                    const float2 ctr = ld2(q);
                     float2 nb[6];
-                    nb[0] = make_float2(xl ? __ldg(m + (q - 1)) : ctr.x, ctr.x);
-                    nb[1] = make_float2(ctr.y, xr ? __ldg(m + (q + 2)) : ctr.y);
-                    nb[2] = ym ? __ldg(reinterpret_cast<const float2*>(m + (q - sy))) : ctr;
-                    nb[3] = yp ? __ldg(reinterpret_cast<const float2*>(m + (q + sy))) : ctr;
-                    nb[4] = zm ? __ldg(reinterpret_cast<const float2*>(m + (q - sz))) : ctr;
-                    nb[5] = zp ? __ldg(reinterpret_cast<const float2*>(m + (q + sz))) : ctr;
+                    nb[0] = make_float2(__ldg(m + (xl ? q - 1 : q)), ctr.x);
+                    nb[1] = make_float2(ctr.y, __ldg(m + (xr ? q + 2 : q + 1)));
+                    nb[2] = ld2(ym ? q - sy : q);
+                    nb[3] = ld2(yp ? q + sy : q);
+                    nb[4] = ld2(zm ? q - sz : q);
+                    nb[5] = ld2(zp ? q + sz : q);
                     mc[c] = ctr;
                     ex[c] = CellPairLLG::exch(ctr, nb);
                 }
