@@ -448,6 +448,9 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
     }
 }
 
+#ifndef MMB_XS_PAIR_STORE
+#define MMB_XS_PAIR_STORE 0 // 3c: one row pair per thread, 16-byte stores (measured slower)
+#endif
 #ifndef MMB_XS_PAIR_LLG
 #define MMB_XS_PAIR_LLG 1 // f32 local terms on packed cell pairs (even nx)
 #endif
@@ -554,21 +557,34 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     const long long cur_step = ctl->cur_step;
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->step = cur_step + 1;
 
-    // ---- 1a. stage the 3*TR convolved half-spectrum rows (async copies). Each thread keeps
-    // one row r and walks kx with a fixed stride (NT is a multiple of 3*TR): no division,
-    // 32-bit element offsets.
-    static_assert(NT % (3 * TR) == 0, "thread count must be a multiple of the tile rows");
-    constexpr int KSTEP = NT / (3 * TR);
-    const int my_r = tid % (3 * TR), my_k0 = tid / (3 * TR);
-    const int my_c = my_r / TR, my_y = y0 + (my_r - my_c * TR);
-    const bool my_live = my_y < ny;
+    // ---- 1a. stage the 3*TR convolved half-spectrum rows (async copies) as TR*3/2 row pairs
+    // (2p, 2p+1) = (y, y+1) of one component, interleaved [p][kx][2]: the two rows stage A
+    // packs into one complex sequence sit next to each other in S (y fastest) and in shared
+    // memory, so a pair moves as one 16-byte copy (f32). Each thread keeps one pair and walks
+    // kx with a fixed stride (NT is a multiple of 3*TR/2): no division, 32-bit offsets.
+    static_assert(TR % 2 == 0, "tile rows come in pairs");
+    constexpr int NPR = 3 * TR / 2, PP = 2 * XH; // row pairs, pair pitch (complex values)
+    static_assert(NT % NPR == 0 && NPR * PP <= X::AREA, "thread count must be a multiple of the row pairs");
+    constexpr int KSTEP = NT / NPR;
+    const int my_p = tid % NPR, my_k0 = tid / NPR;
+    const int my_c = (2 * my_p) / TR, my_y = y0 + (2 * my_p - my_c * TR);
+    const bool live0 = my_y < ny, live1 = my_y + 1 < ny;
+    // even ny: pairs never straddle the grid edge and start 16-byte aligned in S
+    const bool vec = (ny & 1) == 0;
     const int kx_stride = 3 * nz * ny;                      // S elements between kx blocks
     const int row_off = (my_c * nz + z) * ny + my_y;        // (c, z, y) offset inside a kx block
     {
-        cx<T>* dst = sm + my_r * XHP;
+        cx<T>* dst = sm + my_p * PP;
         for (int k = my_k0; k < XH; k += KSTEP) {
-            if (my_live) cp_async<sizeof(cx<T>)>(dst + k, S + (k * kx_stride + row_off));
-            else dst[k] = cx<T>{0, 0};
+            const cx<T>* src = S + (k * kx_stride + row_off);
+            if (live0 && vec) {
+                cp_async_pair<T>(dst + 2 * k, src);
+            } else {
+                if (live0) cp_async<sizeof(cx<T>)>(dst + 2 * k, src);
+                else dst[2 * k] = cx<T>{0, 0};
+                if (live1) cp_async<sizeof(cx<T>)>(dst + 2 * k + 1, src + 1);
+                else dst[2 * k + 1] = cx<T>{0, 0};
+            }
         }
     }
     stage_twiddles<T, LOG2L>(tws, tw);
@@ -583,19 +599,19 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     const bool a_task = ta < P * N1;
     const int pa = ta / N1, n1 = ta % N1;
     if (a_task) {
-        const cx<T>* A = sm + (2 * pa) * XHP;
-        const cx<T>* B = A + XHP;
+        const cx<T>* AB = sm + pa * PP;
 #pragma unroll
         for (int m = 0; m < RA; ++m) {
             const int k = n1 + N1 * (LA * m + ha);
-            cx<T> zv;
+            cx<T> a, b, zv;
             if (k == 0 || 2 * k == L) {
-                zv = cx<T>{A[k].x, B[k].x};
+                ld_pair<T>(AB + 2 * k, a, b);
+                zv = cx<T>{a.x, b.x};
             } else if (2 * k < L) {
-                const cx<T> a = A[k], b = B[k];
+                ld_pair<T>(AB + 2 * k, a, b);
                 zv = cx<T>{a.x - b.y, a.y + b.x};
             } else {
-                const cx<T> a = A[L - k], b = B[L - k];
+                ld_pair<T>(AB + 2 * (L - k), a, b);
                 zv = cx<T>{a.x + b.y, b.x - a.y};
             }
             v[m] = zv;
@@ -828,17 +844,43 @@ llg_done:
         }
     }
     __syncthreads();
-    // ---- 3c. separate the packed rows, write the next step's half spectra (kx-major)
+    // ---- 3c. separate the packed rows, write the next step's half spectra (kx-major), one
+    // row pair per thread as in 1a
     const T half = T(0.5);
-    if (my_live) {
-        const cx<T>* zr = sm + (my_r >> 1) * ZP;
-        const bool odd = my_r & 1;
+#if MMB_XS_PAIR_STORE
+    if (live0) {
+        const cx<T>* zr = sm + my_p * ZP;
         for (int k = my_k0; k < XH; k += KSTEP) {
             const cx<T> zk = zr[k], zm = zr[(L - k) & (L - 1)];
-            S[k * kx_stride + row_off] = odd ? cx<T>{(zk.y + zm.y) * half, (zm.x - zk.x) * half}
-                                             : cx<T>{(zk.x + zm.x) * half, (zk.y - zm.y) * half};
+            const cx<T> e{(zk.x + zm.x) * half, (zk.y - zm.y) * half};
+            const cx<T> o{(zk.y + zm.y) * half, (zm.x - zk.x) * half};
+            cx<T>* d = S + (k * kx_stride + row_off);
+            if (vec) {
+                st_pair<T>(d, e, o);
+            } else {
+                d[0] = e;
+                if (live1) d[1] = o;
+            }
         }
     }
+#else
+    {
+        // one row per thread (odd rows take the imaginary half of their pair's Z row)
+        constexpr int KS1 = NT / (3 * TR);
+        const int r = tid % (3 * TR), k0 = tid / (3 * TR);
+        const int c = r / TR, y = y0 + (r - c * TR);
+        if (y < ny) {
+            const cx<T>* zr = sm + (r >> 1) * ZP;
+            const bool odd = r & 1;
+            const int off = (c * nz + z) * ny + y;
+            for (int k = k0; k < XH; k += KS1) {
+                const cx<T> zk = zr[k], zm = zr[(L - k) & (L - 1)];
+                S[k * kx_stride + off] = odd ? cx<T>{(zk.y + zm.y) * half, (zm.x - zk.x) * half}
+                                             : cx<T>{(zk.x + zm.x) * half, (zk.y - zm.y) * half};
+            }
+        }
+    }
+#endif
 
     // ---- per-CTA torque maximum
     __shared__ double red[NT / 32];
