@@ -57,7 +57,8 @@ def main():
     print(f"# {a.kernel}: {ti:.0f} warp instructions executed, {ts:.0f} stall samples, {len(segs)} phases "
           "(split at block barriers)")
     fp = sum(v for s in segs for o, v in s["ops"].items() if o in ("FFMA", "FADD", "FMUL"))
-    print(f"# FP32 (FFMA/FADD/FMUL) share of all instructions: {fp / ti:.3f}")
+    fp2 = sum(v for s in segs for o, v in s["ops"].items() if o in ("FFMA2", "FADD2", "FMUL2"))
+    print(f"# FP32 share of all instructions: scalar FFMA/FADD/FMUL {fp / ti:.3f}, packed FFMA2/FADD2/FMUL2 {fp2 / ti:.3f}")
     for i, s in enumerate(segs):
         if s["inst"] / ti < 0.005 and s["samples"] / ts < 0.005:
             continue
