@@ -23,6 +23,8 @@
 #include "llg_cell.cuh"
 #include "fast_common.cuh"
 
+#include <cuda.h>
+
 #ifndef MMB_YZ_KPREFETCH
 #define MMB_YZ_KPREFETCH 1 // k_yz (nz > 1): load a pencil's tensor coefficients before its z-DFTs
 #endif
@@ -463,6 +465,8 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
 //   3. x-r2c of the new tile -> the half spectra S for the next step, in place.
 // H_demag never reaches HBM and M_{t+1} is not re-read: per step the x side moves
 // S in + S out + M_t + M_{t+1} instead of three separate passes.
+constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+
 template <int LOG2L, int PB = 128, int TSIZE = 4>
 struct XS {
     using SP = Split<LOG2L>;
@@ -497,6 +501,21 @@ struct XS {
     static constexpr int ZP = (1 << LOG2L) + 1;
     static constexpr int A0 = 3 * TR * XHP, A1 = P * SP::N2 * EX, A2 = P * ZP;
     static constexpr int AREA = A0 > A1 ? (A0 > A2 ? A0 : A2) : (A1 > A2 ? A1 : A2);
+    // staging layout [c][kx][TR] (the tile's TR rows of a component side by side per kx):
+    // a TMA box of TR rows x BOXK kx lands as one contiguous block. NB boxes per component,
+    // BOXK rounded so every box starts 128-byte aligned; KXP = kx pitch of a component.
+    static constexpr int XH = (1 << LOG2L) / 2 + 1;
+    static constexpr int NB = (XH + 255) / 256;
+    static constexpr int BQ = 128 / cgcd(128, TR * 2 * TSIZE); // kx multiple for 128-byte boxes
+    static constexpr int BOXK = ((XH + NB - 1) / NB + BQ - 1) / BQ * BQ;
+    // TMA layout where stage A's 16-byte pair loads stay bank-conflict free (an odd number
+    // of 16-byte units between consecutive kx: f32 tiles of 2 or 14 rows) and at Lx >= 2048
+    // (measured faster despite the conflicts: 1024x1024x32 xstep 1.16 -> 1.10 ms); otherwise
+    // the pairs are staged [p][kx][2] by async copies (Lx = 256 with 8-row tiles: TMA
+    // 55 -> 77 us)
+    static constexpr bool TMA = BOXK <= 256 && 3 * NB * BOXK * TR <= AREA && (TR * 2 * TSIZE) % 16 == 0 &&
+                                (((TR * 2 * TSIZE) / 16) % 2 == 1 || LOG2L >= 11);
+    static constexpr int KXP = TMA ? NB * BOXK : XH;
 };
 template <typename T, int LOG2L, int PB>
 constexpr int xs_smem_bytes() {
@@ -525,15 +544,16 @@ constexpr int xs_min_blocks() {
 template <typename T, int LOG2L, int PB>
 __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T, LOG2L, PB>())
     k_xstep(cx<T>* __restrict__ S, const T* __restrict__ m, T* __restrict__ mout, Geom g,
-            const cx<T>* __restrict__ tw, T coeff, T kan, StepCtl* ctl, double* __restrict__ tpart) {
+            const cx<T>* __restrict__ tw, T coeff, T kan, StepCtl* ctl, double* __restrict__ tpart,
+            const __grid_constant__ CUtensorMap tmS, int use_tma) {
     using SP = Split<LOG2L>;
     using X = XS<LOG2L, PB, sizeof(T)>;
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = X::P, TR = X::TR, NT = X::NT;
     constexpr int XH = L / 2 + 1, XHP = X::XHP, EX = X::EX, ZP = X::ZP;
     using RC = rcx<T, LOG2L>; // register complex type (packed FFMA2 arithmetic for f32, L <= 1024)
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw);
-    T* hm = reinterpret_cast<T*>(smem_raw); // [3*TR][nx] tile: H_demag, then M_{t+1}
+    extern __shared__ __align__(128) unsigned char xs_smem[]; // 128 B: TMA box destinations
+    cx<T>* sm = reinterpret_cast<cx<T>*>(xs_smem);
+    T* hm = reinterpret_cast<T*>(xs_smem); // [3*TR][nx] tile: H_demag, then M_{t+1}
     cx<T>* tws = sm + X::AREA;
 
     // ZFAST (tiles of >= 4 rows): z fastest in the grid, so the CTAs of one y tile in
@@ -557,39 +577,60 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     const long long cur_step = ctl->cur_step;
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->step = cur_step + 1;
 
-    // ---- 1a. stage the 3*TR convolved half-spectrum rows (async copies) as TR*3/2 row pairs
-    // (2p, 2p+1) = (y, y+1) of one component, interleaved [p][kx][2]: the two rows stage A
-    // packs into one complex sequence sit next to each other in S (y fastest) and in shared
-    // memory, so a pair moves as one 16-byte copy (f32). Each thread keeps one pair and walks
-    // kx with a fixed stride (NT is a multiple of 3*TR/2): no division, 32-bit offsets.
+    // ---- 1a. stage the 3*TR convolved half-spectrum rows as [c][kx][TR]: rows 2p, 2p+1 (y,
+    // y+1 of one component), which stage A packs into one complex sequence, sit side by side.
+    // TMA (use_tma): NB boxes of TR y x BOXK kx per component, issued by one thread (rows past
+    // ny and columns past Xh arrive as zeros). Otherwise one 16-byte L1-allocating async copy
+    // per row pair and kx, each thread keeping one pair and walking kx with a fixed stride.
     static_assert(TR % 2 == 0, "tile rows come in pairs");
-    constexpr int NPR = 3 * TR / 2, PP = 2 * XH; // row pairs, pair pitch (complex values)
-    static_assert(NT % NPR == 0 && NPR * PP <= X::AREA, "thread count must be a multiple of the row pairs");
+    constexpr int NPR = 3 * TR / 2, KXP = X::KXP; // row pairs, kx pitch of a component
+    static_assert(NT % NPR == 0 && 3 * KXP * TR <= X::AREA, "thread count must be a multiple of the row pairs");
+    // pair p's value at kx k: sm[pair_base(p) + k * KS]
+    constexpr int KS = X::TMA ? TR : 2;
+    const auto pair_base = [&](int p) {
+        const int c = (2 * p) / TR;
+        return X::TMA ? c * KXP * TR + (2 * p - c * TR) : p * 2 * XH;
+    };
     constexpr int KSTEP = NT / NPR;
     const int my_p = tid % NPR, my_k0 = tid / NPR;
-    const int my_c = (2 * my_p) / TR, my_y = y0 + (2 * my_p - my_c * TR);
+    const int my_c = (2 * my_p) / TR, my_yl = 2 * my_p - my_c * TR, my_y = y0 + my_yl;
     const bool live0 = my_y < ny, live1 = my_y + 1 < ny;
-    // even ny: pairs never straddle the grid edge and start 16-byte aligned in S
-    const bool vec = (ny & 1) == 0;
     const int kx_stride = 3 * nz * ny;                      // S elements between kx blocks
     const int row_off = (my_c * nz + z) * ny + my_y;        // (c, z, y) offset inside a kx block
-    {
-        cx<T>* dst = sm + my_p * PP;
+    __shared__ __align__(8) unsigned long long sbar;
+    const bool tma = X::TMA && use_tma;
+    if (tma) {
+        if (tid == 0) {
+            mbar_init(&sbar, 1);
+            mbar_expect_tx(&sbar, 3u * X::NB * X::BOXK * TR * static_cast<unsigned>(sizeof(cx<T>)));
+            constexpr int E = static_cast<int>(sizeof(cx<T>)) / 8; // 8-byte map elements
+#pragma unroll 1
+            for (int c = 0; c < 3; ++c)
+#pragma unroll 1
+                for (int j = 0; j < X::NB; ++j)
+                    tma_load_3d(sm + (c * KXP + j * X::BOXK) * TR, &tmS, y0 * E, c * nz + z, j * X::BOXK, &sbar);
+        }
+    } else {
+        // even ny: pairs never straddle the grid edge and start 16-byte aligned in S
+        const bool vec = (ny & 1) == 0;
+        cx<T>* dst = sm + pair_base(my_p);
         for (int k = my_k0; k < XH; k += KSTEP) {
             const cx<T>* src = S + (k * kx_stride + row_off);
+            cx<T>* d = dst + k * KS;
             if (live0 && vec) {
-                cp_async_pair<T>(dst + 2 * k, src);
+                cp_async_pair<T>(d, src);
             } else {
-                if (live0) cp_async<sizeof(cx<T>)>(dst + 2 * k, src);
-                else dst[2 * k] = cx<T>{0, 0};
-                if (live1) cp_async<sizeof(cx<T>)>(dst + 2 * k + 1, src + 1);
-                else dst[2 * k + 1] = cx<T>{0, 0};
+                if (live0) cp_async<sizeof(cx<T>)>(d, src);
+                else d[0] = cx<T>{0, 0};
+                if (live1) cp_async<sizeof(cx<T>)>(d + 1, src + 1);
+                else d[1] = cx<T>{0, 0};
             }
         }
     }
     stage_twiddles<T, LOG2L>(tws, tw);
     cp_async_wait_all();
     __syncthreads();
+    if (tma) mbar_wait(&sbar, 0);
 
     // ---- 1b. inverse stage A on Z = A + iB (rows 2p, 2p+1 of the same component); lane
     // h of a pair task takes n2 = LA m + h
@@ -599,19 +640,19 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     const bool a_task = ta < P * N1;
     const int pa = ta / N1, n1 = ta % N1;
     if (a_task) {
-        const cx<T>* AB = sm + pa * PP;
+        const cx<T>* AB = sm + pair_base(pa);
 #pragma unroll
         for (int m = 0; m < RA; ++m) {
             const int k = n1 + N1 * (LA * m + ha);
             cx<T> a, b, zv;
             if (k == 0 || 2 * k == L) {
-                ld_pair<T>(AB + 2 * k, a, b);
+                ld_pair<T>(AB + k * KS, a, b);
                 zv = cx<T>{a.x, b.x};
             } else if (2 * k < L) {
-                ld_pair<T>(AB + 2 * k, a, b);
+                ld_pair<T>(AB + k * KS, a, b);
                 zv = cx<T>{a.x - b.y, a.y + b.x};
             } else {
-                ld_pair<T>(AB + 2 * (L - k), a, b);
+                ld_pair<T>(AB + (L - k) * KS, a, b);
                 zv = cx<T>{a.x + b.y, b.x - a.y};
             }
             v[m] = zv;
@@ -1069,17 +1110,54 @@ int fast_xstep_blocks(const Geom& g) {
     }
 }
 
+// TMA descriptor of the kx-major half spectra S for the x tiles: 3-D (y, (c, z) row, kx) in
+// 8-byte elements, box TR y x 1 row x BOXK kx. False (plain async copies instead) when the
+// driver entry point is missing, MMB_XS_TMA=0, or the layout breaks TMA's 16-byte rules.
+template <typename T>
+bool xs_tensor_map(CUtensorMap* tm, const cx<T>* S, const Geom& g, int tr, int boxk) {
+    static const bool off = [] {
+        const char* e = std::getenv("MMB_XS_TMA");
+        return e && e[0] == '0';
+    }();
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static const Encode encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<Encode>(nullptr);
+        return reinterpret_cast<Encode>(fn);
+    }();
+    if (off || !encode) return false;
+    const int e = static_cast<int>(sizeof(cx<T>)) / 8;
+    const unsigned long long esz = sizeof(cx<T>);
+    if ((g.ny * esz) % 16 != 0 || (reinterpret_cast<unsigned long long>(S) & 15u) != 0) return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.ny) * e, static_cast<cuuint64_t>(3 * g.nz),
+                                static_cast<cuuint64_t>(g.xh)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.ny) * esz, static_cast<cuuint64_t>(3 * g.nz) * g.ny * esz};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(tr * e), 1u, static_cast<cuuint32_t>(boxk)};
+    const cuuint32_t es[3] = {1u, 1u, 1u};
+    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<cx<T>*>(S), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T>
 void launch_fast_xstep(cx<T>* S, const T* m, T* mout, const Geom& g, const cx<T>* tw,
                        double exch_coeff, double aniso_coeff, StepCtl* ctl, double* tpart,
                        cudaStream_t stream, bool pdl) {
     const T coeff = static_cast<T>(exch_coeff), kan = static_cast<T>(aniso_coeff);
     switch (g.log2lx) {
-#define X(l) case l: if (xstep_small<l>(g)) { const dim3 grid = xs_grid<XS<l, 16>>(g); \
-        launch_pdl(pdl, k_xstep<T, l, 16>, grid, XS<l, 16, sizeof(T)>::NT, xs_smem_bytes<T, l, 16>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); \
-        } else { if (xs_smem_bytes<T, l, xs_pb(l)>() > 227 * 1024) throw std::invalid_argument("fast path: x tile exceeds shared memory"); \
-        const dim3 grid = xs_grid<XS<l, xs_pb(l)>>(g); \
-        launch_pdl(pdl, k_xstep<T, l, xs_pb(l)>, grid, XS<l, xs_pb(l), sizeof(T)>::NT, xs_smem_bytes<T, l, xs_pb(l)>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart); } break;
+#define X(l) case l: if (xstep_small<l>(g)) { using XA = XS<l, 16, sizeof(T)>; const dim3 grid = xs_grid<XA>(g); \
+        CUtensorMap tm{}; const int ut = XA::TMA && xs_tensor_map<T>(&tm, S, g, XA::TR, XA::BOXK); \
+        launch_pdl(pdl, k_xstep<T, l, 16>, grid, XA::NT, xs_smem_bytes<T, l, 16>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart, tm, ut); \
+        } else { using XB = XS<l, xs_pb(l), sizeof(T)>; \
+        if (xs_smem_bytes<T, l, xs_pb(l)>() > 227 * 1024) throw std::invalid_argument("fast path: x tile exceeds shared memory"); \
+        const dim3 grid = xs_grid<XB>(g); \
+        CUtensorMap tm{}; const int ut = XB::TMA && xs_tensor_map<T>(&tm, S, g, XB::TR, XB::BOXK); \
+        launch_pdl(pdl, k_xstep<T, l, xs_pb(l)>, grid, XB::NT, xs_smem_bytes<T, l, xs_pb(l)>(), stream, S, m, mout, g, tw, coeff, kan, ctl, tpart, tm, ut); } break;
         MMB_FAST_CASES(X)
 #undef X
         default: throw std::invalid_argument("fast path: bad Lx");
