@@ -146,7 +146,8 @@ constexpr int z_smem_bytes() {
 
 template <typename T, int LOG2LZ>
 __global__ void __launch_bounds__(kZThreads)
-    k_zmac(cx<T>* __restrict__ S2, Geom g, const cx<T>* __restrict__ tw, const T* __restrict__ kt) {
+    k_zmac(cx<T>* __restrict__ S2, Geom g, const cx<T>* __restrict__ tw, const T* __restrict__ kt,
+           const __grid_constant__ CUtensorMap tm, int use_tma) {
     // Lz = N1*N2. Forward: stage A (DFT_N2 over n2 per (c, n1)), then the fused middle: per
     // (k2, ky) all three components in registers, DFT_N1 -> kz = k2 + N2 k1 natural, tensor
     // MAC, inverse DFT_N1, conj twiddle; then inverse stage A' (IDFT_N2 per (c, n1)) straight
@@ -154,8 +155,8 @@ __global__ void __launch_bounds__(kZThreads)
     using SP = Split<LOG2LZ>;
     constexpr int LZ = SP::L, N1 = SP::N1, N2 = SP::N2, W = zw<T, LOG2LZ>();
     constexpr int CS = LZ * W; // component stride in a tile buffer
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    cx<T>* A = reinterpret_cast<cx<T>*>(smem_raw); // [c][z][w]
+    extern __shared__ __align__(128) unsigned char zm_smem[]; // 128 B: TMA box destinations
+    cx<T>* A = reinterpret_cast<cx<T>*>(zm_smem); // [c][z][w]
     cx<T>* B = A + 3 * CS;
     cx<T>* tws = B + 3 * CS;
     const int kx = blockIdx.y, ky0 = blockIdx.x * W;
@@ -193,12 +194,25 @@ __global__ void __launch_bounds__(kZThreads)
             }
         }
     };
-    constexpr int VEC16 = 16 / static_cast<int>(sizeof(cx<T>));
-    if (VEC16 > 1 && wl == W && (ly % VEC16) == 0) load_tile(std::integral_constant<int, VEC16>{});
-    else load_tile(std::integral_constant<int, 1>{});
+    __shared__ __align__(8) unsigned long long zbar;
+    if (use_tma) {
+        // one TMA box per component: W ky x nz planes of row (c, 0..nz) at kx -> A[c][z][w]
+        // (the planes z >= nz of the tile are never read; ky past Ly arrive as zeros)
+        if (tid == 0) {
+            mbar_init(&zbar, 1);
+            mbar_expect_tx(&zbar, 3u * nz * W * static_cast<unsigned>(sizeof(cx<T>)));
+            constexpr int E = static_cast<int>(sizeof(cx<T>)) / 8;
+            for (int c = 0; c < 3; ++c) tma_load_3d(A + c * CS, &tm, ky0 * E, c * nz, kx, &zbar);
+        }
+    } else {
+        constexpr int VEC16 = 16 / static_cast<int>(sizeof(cx<T>));
+        if (VEC16 > 1 && wl == W && (ly % VEC16) == 0) load_tile(std::integral_constant<int, VEC16>{});
+        else load_tile(std::integral_constant<int, 1>{});
+    }
     stage_twiddles<T, LOG2LZ>(tws, tw);
     cp_async_wait_all();
     __syncthreads();
+    if (use_tma) mbar_wait(&zbar, 0);
 
     // forward stage A: task (c, n1, w); planes z >= nz are zero (pruned, never read)
     for (int t = tid; t < 3 * N1 * W; t += kZThreads) {
@@ -377,9 +391,14 @@ void launch_big_yi(const cx<T>* S2, cx<T>* S, const Geom& g, const cx<T>* tw, cu
 
 template <typename T>
 void launch_big_z(cx<T>* S2, const Geom& g, const cx<T>* tw, const T* kt, cudaStream_t stream) {
+    static const bool tma_off = env_off("MMB_ZMAC_TMA");
+    const unsigned long long e = sizeof(cx<T>) / 8, esz = sizeof(cx<T>);
     switch (g.log2lz) {
-#define X(l) case l: { const dim3 grid((g.ly + zw<T, l>() - 1) / zw<T, l>(), g.xh); \
-        k_zmac<T, l><<<grid, kZThreads, z_smem_bytes<T, l>(), stream>>>(S2, g, tw, kt); break; }
+#define X(l) case l: { constexpr int W = zw<T, l>(); const dim3 grid((g.ly + W - 1) / W, g.xh); \
+        CUtensorMap tm{}; \
+        const int ut = !tma_off && g.nz <= 256 && make_tmap_3d(&tm, S2, g.ly * e, 3ull * g.nz, g.xh, g.ly * esz, \
+                                                   3ull * g.nz * g.ly * esz, static_cast<unsigned>(W * e), static_cast<unsigned>(g.nz), 1u); \
+        k_zmac<T, l><<<grid, kZThreads, z_smem_bytes<T, l>(), stream>>>(S2, g, tw, kt, tm, ut); break; }
         MMB_Z_CASES(X)
 #undef X
         default: throw std::invalid_argument("big path: bad Lz");

@@ -6,7 +6,48 @@
 #include "fft4.cuh"
 #include "types.cuh"
 
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
 namespace mmb {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda), or null
+using TmapEncode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline TmapEncode tmap_encoder() {
+    static const TmapEncode encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<TmapEncode>(nullptr);
+        return reinterpret_cast<TmapEncode>(fn);
+    }();
+    return encode;
+}
+// 3-D tile map over 8-byte elements: dims innermost first, byte strides of dims 1 and 2.
+// False when the layout breaks TMA's rules (16-byte base and strides) or TMA is unavailable.
+inline bool make_tmap_3d(CUtensorMap* tm, const void* base, unsigned long long d0, unsigned long long d1,
+                         unsigned long long d2, unsigned long long s1, unsigned long long s2, unsigned b0,
+                         unsigned b1, unsigned b2) {
+    const TmapEncode encode = tmap_encoder();
+    if (!encode || (reinterpret_cast<unsigned long long>(base) & 15u) || (s1 & 15u) || (s2 & 15u) || (b0 * 8u) % 16u)
+        return false;
+    const cuuint64_t dims[3] = {d0, d1, d2};
+    const cuuint64_t strides[2] = {s1, s2};
+    const cuuint32_t box[3] = {b0, b1, b2};
+    const cuuint32_t es[3] = {1u, 1u, 1u};
+    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+inline bool env_off(const char* name) {
+    const char* e = std::getenv(name);
+    return e && e[0] == '0';
+}
 
 __device__ __forceinline__ long long sf_row(int kx, int c, int z, int nz, int ny) {
     return ((static_cast<long long>(kx) * 3 + c) * nz + z) * ny;

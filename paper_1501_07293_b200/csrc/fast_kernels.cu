@@ -23,8 +23,6 @@
 #include "llg_cell.cuh"
 #include "fast_common.cuh"
 
-#include <cuda.h>
-
 #ifndef MMB_YZ_KPREFETCH
 #define MMB_YZ_KPREFETCH 1 // k_yz (nz > 1): load a pencil's tensor coefficients before its z-DFTs
 #endif
@@ -1115,33 +1113,10 @@ int fast_xstep_blocks(const Geom& g) {
 // driver entry point is missing, MMB_XS_TMA=0, or the layout breaks TMA's 16-byte rules.
 template <typename T>
 bool xs_tensor_map(CUtensorMap* tm, const cx<T>* S, const Geom& g, int tr, int boxk) {
-    static const bool off = [] {
-        const char* e = std::getenv("MMB_XS_TMA");
-        return e && e[0] == '0';
-    }();
-    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static const Encode encode = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return static_cast<Encode>(nullptr);
-        return reinterpret_cast<Encode>(fn);
-    }();
-    if (off || !encode) return false;
-    const int e = static_cast<int>(sizeof(cx<T>)) / 8;
-    const unsigned long long esz = sizeof(cx<T>);
-    if ((g.ny * esz) % 16 != 0 || (reinterpret_cast<unsigned long long>(S) & 15u) != 0) return false;
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.ny) * e, static_cast<cuuint64_t>(3 * g.nz),
-                                static_cast<cuuint64_t>(g.xh)};
-    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.ny) * esz, static_cast<cuuint64_t>(3 * g.nz) * g.ny * esz};
-    const cuuint32_t box[3] = {static_cast<cuuint32_t>(tr * e), 1u, static_cast<cuuint32_t>(boxk)};
-    const cuuint32_t es[3] = {1u, 1u, 1u};
-    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<cx<T>*>(S), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    static const bool off = env_off("MMB_XS_TMA");
+    const unsigned long long e = sizeof(cx<T>) / 8, esz = sizeof(cx<T>);
+    return !off && make_tmap_3d(tm, S, g.ny * e, 3ull * g.nz, g.xh, g.ny * esz, 3ull * g.nz * g.ny * esz,
+                                static_cast<unsigned>(tr * e), 1u, static_cast<unsigned>(boxk));
 }
 
 template <typename T>
