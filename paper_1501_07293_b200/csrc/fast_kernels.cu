@@ -595,18 +595,21 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     const bool live0 = my_y < ny, live1 = my_y + 1 < ny;
     const int kx_stride = 3 * nz * ny;                      // S elements between kx blocks
     const int row_off = (my_c * nz + z) * ny + my_y;        // (c, z, y) offset inside a kx block
-    __shared__ __align__(8) unsigned long long sbar;
+    // one transaction barrier per component: the stage-A tasks of component c start as soon
+    // as its boxes land, while the later components are still in flight
+    __shared__ __align__(8) unsigned long long sbar[3];
     const bool tma = X::TMA && use_tma;
     if (tma) {
         if (tid == 0) {
-            mbar_init(&sbar, 1);
-            mbar_expect_tx(&sbar, 3u * X::NB * X::BOXK * TR * static_cast<unsigned>(sizeof(cx<T>)));
             constexpr int E = static_cast<int>(sizeof(cx<T>)) / 8; // 8-byte map elements
 #pragma unroll 1
-            for (int c = 0; c < 3; ++c)
+            for (int c = 0; c < 3; ++c) {
+                mbar_init(&sbar[c], 1);
+                mbar_expect_tx(&sbar[c], X::NB * X::BOXK * TR * static_cast<unsigned>(sizeof(cx<T>)));
 #pragma unroll 1
                 for (int j = 0; j < X::NB; ++j)
-                    tma_load_3d(sm + (c * KXP + j * X::BOXK) * TR, &tmS, y0 * E, c * nz + z, j * X::BOXK, &sbar);
+                    tma_load_3d(sm + (c * KXP + j * X::BOXK) * TR, &tmS, y0 * E, c * nz + z, j * X::BOXK, &sbar[c]);
+            }
         }
     } else {
         // even ny: pairs never straddle the grid edge and start 16-byte aligned in S
@@ -628,7 +631,6 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     stage_twiddles<T, LOG2L>(tws, tw);
     cp_async_wait_all();
     __syncthreads();
-    if (tma) mbar_wait(&sbar, 0);
 
     // ---- 1b. inverse stage A on Z = A + iB (rows 2p, 2p+1 of the same component); lane
     // h of a pair task takes n2 = LA m + h
@@ -638,6 +640,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     const bool a_task = ta < P * N1;
     const int pa = ta / N1, n1 = ta % N1;
     if (a_task) {
+        if (tma) mbar_wait(&sbar[(2 * pa) / TR], 0); // every component has stage-A tasks
         const cx<T>* AB = sm + pair_base(pa);
 #pragma unroll
         for (int m = 0; m < RA; ++m) {
