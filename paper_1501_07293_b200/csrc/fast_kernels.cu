@@ -252,7 +252,10 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
 
     const int nz = g.nz, ny = g.ny, xh = g.xh;
     cx<T>* tws = sm + kxb * 3 * nz * RP;
-    __shared__ __align__(8) unsigned long long bar;
+    // one transaction barrier per y-forward batch of rows (the last one takes the rest): a
+    // batch's stage A starts when its rows land
+    constexpr int NBAR = 4;
+    __shared__ __align__(8) unsigned long long bar[NBAR];
     pdl_wait();
     pdl_trigger(); // after the wait: at most one kernel ahead of the running one
     if (prologue && blockIdx.x == 0 && threadIdx.x == 0) step_prologue(ctl, st, prologue);
@@ -276,10 +279,13 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
     const unsigned rowbytes = static_cast<unsigned>(ny * sizeof(cx<T>));
     const bool bulk = (rowbytes % 16) == 0 && (!PEER || rm.local);
     if (tid == 0) {
-        mbar_init(&bar, 1);
+        for (int b = 0; b < NBAR; ++b) mbar_init(&bar[b], 1);
         if (bulk) {
-            mbar_expect_tx(&bar, rowbytes * rows);
-            for (int r = 0; r < rows; ++r) bulk_g2s(sm + r * RP, grow(r), rowbytes, &bar);
+            for (int b = 0; b < NBAR; ++b) {
+                const int r0 = b * RB, r1 = b == NBAR - 1 ? rows : min(rows, r0 + RB);
+                if (r1 > r0) mbar_expect_tx(&bar[b], rowbytes * (r1 - r0));
+            }
+            for (int r = 0; r < rows; ++r) bulk_g2s(sm + r * RP, grow(r), rowbytes, &bar[min(r / RB, NBAR - 1)]);
         }
     }
     stage_twiddles<T, LOG2L>(tws, tw);
@@ -288,7 +294,6 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
     }
     cp_async_wait_all();
     __syncthreads();
-    if (bulk) mbar_wait(&bar, 0);
 
     // ---- y forward, batches of RB rows
     for (int rb0 = 0; rb0 < rows; rb0 += RB) {
@@ -296,6 +301,7 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
         RC v[N2];
         const int ra = rb0 + tid / N1, n1 = tid % N1;
         const bool a_task = tid < nb * N1;
+        if (bulk && rb0 / RB < NBAR) mbar_wait(&bar[rb0 / RB], 0);
         if (a_task) {
             const cx<T>* src = sm + ra * RP;
             constexpr int NZ = L == 1 ? 1 : N2 / 2;
