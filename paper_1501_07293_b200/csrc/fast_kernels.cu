@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
 }
 
 #ifndef MMB_XS_PAIR_STORE
-#define MMB_XS_PAIR_STORE 0 // 3c: one row pair per thread, 16-byte stores (measured slower)
+#define MMB_XS_PAIR_STORE 0 // 3c: one row pair per thread, 16-byte stores (measured +0.5 us on k_xstep)
 #endif
 #ifndef MMB_XS_PAIR_LLG
 #define MMB_XS_PAIR_LLG 1 // f32 local terms on packed cell pairs (even nx)
@@ -603,6 +603,8 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     const int row_off = (my_c * nz + z) * ny + my_y;        // (c, z, y) offset inside a kx block
     // one transaction barrier per component: the stage-A tasks of component c start as soon
     // as its boxes land, while the later components are still in flight
+    // even ny: pairs never straddle the grid edge and start 16-byte aligned in S
+    const bool vec = (ny & 1) == 0;
     __shared__ __align__(8) unsigned long long sbar[3];
     const bool tma = X::TMA && use_tma;
     if (tma) {
@@ -618,8 +620,6 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
             }
         }
     } else {
-        // even ny: pairs never straddle the grid edge and start 16-byte aligned in S
-        const bool vec = (ny & 1) == 0;
         cx<T>* dst = sm + pair_base(my_p);
         for (int k = my_k0; k < XH; k += KSTEP) {
             const cx<T>* src = S + (k * kx_stride + row_off);
