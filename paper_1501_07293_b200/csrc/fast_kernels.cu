@@ -311,16 +311,15 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
                 v[n2] = y < ny ? RC(src[y]) : RC{0, 0};
             }
             DftP<N2, -1, NZ, N2>::run(v);
+            // twiddles before the barrier: their shared loads overlap the other warps' arrival
+#pragma unroll
+            for (int k2 = 1; k2 < N2; ++k2) v[k2] = cmul(v[k2], RC(tws[k2 * N1 + n1]));
         }
         __syncthreads(); // the staged input rows are overwritten in place below
         if (a_task) {
             cx<T>* dst = sm + ra * RP;
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) {
-                RC w = v[k2];
-                if (k2 > 0) w = cmul(w, RC(tws[k2 * N1 + n1]));
-                dst[fpad<LOG2L>(k2 * N1 + n1)] = w;
-            }
+            for (int k2 = 0; k2 < N2; ++k2) dst[fpad<LOG2L>(k2 * N1 + n1)] = v[k2];
         }
         __syncthreads();
         const int rbr = rb0 + tid / N2, k2 = tid % N2;
@@ -424,16 +423,14 @@ __global__ void __launch_bounds__(yz_threads<T, LOG2L>())
 #pragma unroll
             for (int n2 = 0; n2 < N2; ++n2) v[n2] = src[fpad<LOG2L>(n1 + N1 * n2)];
             DftP<N2, +1, N2, N2>::run(v);
+#pragma unroll
+            for (int k2 = 1; k2 < N2; ++k2) v[k2] = cmulc(v[k2], RC(tws[k2 * N1 + n1]));
         }
         __syncthreads();
         if (a_task) {
             cx<T>* dst = sm + ra * RP;
 #pragma unroll
-            for (int k2 = 0; k2 < N2; ++k2) {
-                RC w = v[k2];
-                if (k2 > 0) w = cmulc(w, RC(tws[k2 * N1 + n1]));
-                dst[fpad<LOG2L>(k2 * N1 + n1)] = w;
-            }
+            for (int k2 = 0; k2 < N2; ++k2) dst[fpad<LOG2L>(k2 * N1 + n1)] = v[k2];
         }
         __syncthreads();
         const int rbr = rb0 + tid / N2, k2 = tid % N2;
@@ -555,6 +552,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
     constexpr int L = SP::L, N1 = SP::N1, N2 = SP::N2, P = X::P, TR = X::TR, NT = X::NT;
     constexpr int XH = L / 2 + 1, XHP = X::XHP, EX = X::EX, ZP = X::ZP;
     using RC = rcx<T, LOG2L>; // register complex type (packed FFMA2 arithmetic for f32, L <= 1024)
+    constexpr bool TWPRE = PB <= 16; // stage-A twiddles before the barrier (small tiles)
     extern __shared__ __align__(128) unsigned char xs_smem[]; // 128 B: TMA box destinations
     cx<T>* sm = reinterpret_cast<cx<T>*>(xs_smem);
     T* hm = reinterpret_cast<T*>(xs_smem); // [3*TR][nx] tile: H_demag, then M_{t+1}
@@ -666,6 +664,15 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
         }
         if constexpr (LA == 2) dft_pair<RA, +1, RA>(v, ha);
         else DftP<N2, +1, N2, N2>::run(v);
+        // small tiles: twiddles before the barrier, their shared loads overlapping the other
+        // warps' arrival (256^2 film 14.8 -> 13.3 us; the large tiles measured slower)
+        if constexpr (TWPRE) {
+#pragma unroll
+            for (int kk = 0; kk < RA; ++kk) {
+                const int k2 = kk + RA * ha;
+                if (k2 > 0) v[kk] = cmulc(v[kk], RC(tws[k2 * N1 + n1]));
+            }
+        }
     }
     __syncthreads();
     if (a_task) {
@@ -674,7 +681,7 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
         for (int kk = 0; kk < RA; ++kk) {
             const int k2 = kk + RA * ha;
             RC w = v[kk];
-            if (k2 > 0) w = cmulc(w, RC(tws[k2 * N1 + n1]));
+            if (!TWPRE && k2 > 0) w = cmulc(w, RC(tws[k2 * N1 + n1]));
             ex[k2 * EX] = w;
         }
     }
@@ -857,6 +864,13 @@ llg_done:
         }
         if constexpr (LA == 2) dft_pair<RA, -1, NZ>(v, ha);
         else DftP<N2, -1, NZ, N2>::run(v);
+        if constexpr (TWPRE) {
+#pragma unroll
+            for (int kk = 0; kk < RA; ++kk) {
+                const int k2 = kk + RA * ha;
+                if (k2 > 0) v[kk] = cmul(v[kk], RC(tws[k2 * N1 + n1]));
+            }
+        }
     }
     __syncthreads(); // the exchange buffer overlays the tile
     if (a_task) {
@@ -865,7 +879,7 @@ llg_done:
         for (int kk = 0; kk < RA; ++kk) {
             const int k2 = kk + RA * ha;
             RC w = v[kk];
-            if (k2 > 0) w = cmul(w, RC(tws[k2 * N1 + n1]));
+            if (!TWPRE && k2 > 0) w = cmul(w, RC(tws[k2 * N1 + n1]));
             ex[k2 * EX] = w;
         }
     }
