@@ -391,7 +391,7 @@ void launch_big_yi(const cx<T>* S2, cx<T>* S, const Geom& g, const cx<T>* tw, cu
 
 template <typename T>
 void launch_big_z(cx<T>* S2, const Geom& g, const cx<T>* tw, const T* kt, cudaStream_t stream) {
-    static const bool tma_off = env_off("MMB_ZMAC_TMA");
+    const bool tma_off = env_off("MMB_ZMAC_TMA"); // read per launch (graph capture): A/B in one process
     const unsigned long long e = sizeof(cx<T>) / 8, esz = sizeof(cx<T>);
     switch (g.log2lz) {
 #define X(l) case l: { constexpr int W = zw<T, l>(); const dim3 grid((g.ly + W - 1) / W, g.xh); \
@@ -422,8 +422,9 @@ std::string big_describe(const Geom& g) {
         MMB_Z_CASES(X)
 #undef X
     }
-    std::snprintf(buf, sizeof buf, "k_yrow<L%d> %s rows/cta=%d ctas=%lld; k_zmac<Lz%d> pencils/cta=%d", g.log2ly,
-                  la == 2 ? "pair" : "plain", p, (nrows + p - 1) / (p ? p : 1), g.log2lz, w);
+    const bool tma = !env_off("MMB_ZMAC_TMA") && tmap_encoder() && (g.ly * sizeof(cx<T>)) % 16 == 0;
+    std::snprintf(buf, sizeof buf, "k_yrow<L%d> %s rows/cta=%d ctas=%lld; k_zmac<Lz%d> pencils/cta=%d tiles=%s", g.log2ly,
+                  la == 2 ? "pair" : "plain", p, (nrows + p - 1) / (p ? p : 1), g.log2lz, w, tma ? "tma" : "copies");
     return buf;
 }
 

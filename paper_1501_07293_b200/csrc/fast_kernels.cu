@@ -1136,7 +1136,7 @@ int fast_xstep_blocks(const Geom& g) {
 // driver entry point is missing, MMB_XS_TMA=0, or the layout breaks TMA's 16-byte rules.
 template <typename T>
 bool xs_tensor_map(CUtensorMap* tm, const cx<T>* S, const Geom& g, int tr, int boxk) {
-    static const bool off = env_off("MMB_XS_TMA");
+    const bool off = env_off("MMB_XS_TMA"); // read per launch (graph capture): A/B in one process
     const unsigned long long e = sizeof(cx<T>) / 8, esz = sizeof(cx<T>);
     return !off && make_tmap_3d(tm, S, g.ny * e, 3ull * g.nz, g.xh, g.ny * esz, 3ull * g.nz * g.ny * esz,
                                 static_cast<unsigned>(tr * e), 1u, static_cast<unsigned>(boxk));
@@ -1182,9 +1182,11 @@ std::string fast_describe(const Geom& g) {
 #define X(l) case l: { const bool sm = xstep_small<l>(g); \
         using XA = XS<l, 16, sizeof(T)>; using XB = XS<l, xs_pb(l), sizeof(T)>; \
         const dim3 gr = sm ? xs_grid<XA>(g) : xs_grid<XB>(g); \
-        std::snprintf(buf, sizeof buf, "k_xstep<L%d,PB%d> tr=%d nt=%d %s grid=%ux%u", l, sm ? 16 : xs_pb(l), \
+        const bool tma = (sm ? XA::TMA : XB::TMA) && !env_off("MMB_XS_TMA") && tmap_encoder() && (g.ny * sizeof(cx<T>)) % 16 == 0; \
+        std::snprintf(buf, sizeof buf, "k_xstep<L%d,PB%d> tr=%d nt=%d %s grid=%ux%u staging=%s", l, sm ? 16 : xs_pb(l), \
                       sm ? XA::TR : XB::TR, sm ? XA::NT : XB::NT, \
-                      (sm ? XA::PAIR : XB::PAIR) ? "pair" : ((sm ? XA::WIDE : XB::WIDE) ? "wide" : "plain"), gr.x, gr.y); \
+                      (sm ? XA::PAIR : XB::PAIR) ? "pair" : ((sm ? XA::WIDE : XB::WIDE) ? "wide" : "plain"), gr.x, gr.y, \
+                      tma ? "tma" : "copies"); \
         xs = buf; break; }
         MMB_FAST_CASES(X)
 #undef X

@@ -406,6 +406,34 @@ def test_wide_x_tile_steps_match_general_path(grid, monkeypatch):
     assert rel(out["fast"], out["general"].astype(np.float64)) <= 1e-5
 
 
+@pytest.mark.parametrize("grid,env", [((512, 512, 8, 1.0), "MMB_XS_TMA"), ((166, 42, 1, 2.5), "MMB_XS_TMA"),
+                                      ((600, 300, 8, 1.0), "MMB_XS_TMA"), ((40, 600, 9, 1.0), "MMB_ZMAC_TMA"),
+                                      ((700, 20, 1, 2.0), "MMB_XS_TMA")])
+def test_tma_staging_bitwise_equals_async_copies(grid, env, monkeypatch):
+    """The TMA tensor-box staging (k_xstep half spectra: 14-row, 2-row and Lx = 2048 tiles;
+    k_zmac pencil tiles) moves the same bytes as the per-thread async copies it replaced:
+    3 steps and the demag field are bitwise equal with the copies forced (env = 0)."""
+    for v in ("MMB_GENERAL_PATH", "MMB_BIG_PATH", "MMB_XS_TMA", "MMB_ZMAC_TMA"):
+        monkeypatch.delenv(v, raising=False)
+    nx, ny, nz, delta = grid
+    sp = spec(nx, ny, nz, delta, 1e7, 1000.0, 100.0, 0.5, 1e-5, [(0, 2, (10.0, -20.0, 5.0))])
+    rng = np.random.default_rng(11)
+    v = rng.uniform(-1, 1, (3, nz, ny, nx))
+    m0 = (1000.0 * v / np.sqrt((v * v).sum(0))).astype(np.float32)
+    out = {}
+    for mode in ("tma", "copies"):
+        if mode == "copies":
+            monkeypatch.setenv(env, "0")
+        sim = b200(sp, "f32")
+        want = ("staging=" if env == "MMB_XS_TMA" else "tiles=") + ("tma" if mode == "tma" else "copies")
+        assert want in sim.path_info(), sim.path_info()
+        sim.set_magnetization(m0)
+        sim.step(3)
+        out[mode] = (sim.magnetization(), sim.demag_field(m0))
+    assert np.array_equal(out["tma"][0], out["copies"][0])
+    assert np.array_equal(out["tma"][1], out["copies"][1])
+
+
 def test_reference_side_adapter_runs():
     """The SimulationBase adapter (integration/b200_simulation.hpp), prebuilt here by the CPU
     suite, drives the B200 path through the C-ABI: 10 steps, 2 cadence records."""
