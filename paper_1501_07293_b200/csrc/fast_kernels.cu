@@ -720,7 +720,6 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
             }
         }
     }
-    __syncthreads();
 
     // ---- 2. local terms + LLG on the tile's cells; M_{t+1} to HBM and to the tile
     CellLLG<T> cl;
@@ -737,42 +736,61 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
             // CellLLG per cell). Every pair offset is even, so the centre, +-y and +-z loads,
             // the H_demag reads and the stores are 8-byte vectors; the outer x neighbours are
             // scalar loads from the same sectors. A missing neighbour is the cell's own centre
-            // (adds +0 to the exchange sum).
+            // (adds +0 to the exchange sum), loaded from the centre's address so every load is
+            // unconditional and independent of the centre load.
+            // Software-pipelined: a pair's 21 loads are in flight while the previous pair
+            // updates, and the first pair's before the barrier that ends the x-inverse.
             CellPairLLG pl;
             pl.load(ctl, coeff, kan);
             const int nxh = nx >> 1;
+            const int hc = (TR * nx) >> 1; // float2 stride between the component tiles
+            float2 rc[3], rn[3][6];
+            const auto load_pair = [&](int yl_, int ip_) {
+                const int j_ = y0 + yl_, i_ = 2 * ip_;
+                const int f_ = z * sz + j_ * sy + i_;
+                const bool xl = i_ > 0, xr = i_ + 2 < nx, ym = j_ > 0, yp = j_ + 1 < ny, zm = zg > 0,
+                           zp = zg + 1 < nzg;
+                const auto ld2 = [&](int o) { return __ldg(reinterpret_cast<const float2*>(m + o)); };
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int q = c * csi + f_;
+                    rc[c] = ld2(q);
+                    rn[c][0].x = __ldg(m + (xl ? q - 1 : q));
+                    rn[c][1].y = __ldg(m + (xr ? q + 2 : q + 1));
+                    rn[c][2] = ld2(ym ? q - sy : q);
+                    rn[c][3] = ld2(yp ? q + sy : q);
+                    rn[c][4] = ld2(zm ? q - sz : q);
+                    rn[c][5] = ld2(zp ? q + sz : q);
+                }
+            };
             int yl = 0, ip = tid;
             while (ip >= nxh) {
                 ip -= nxh;
                 ++yl;
             }
-            for (; yl < TR; ) {
-                const int j = y0 + yl;
-                if (j >= ny) break;
-                const int i = 2 * ip;
+            bool valid = yl < TR && y0 + yl < ny;
+            if (valid) load_pair(yl, ip);
+            __syncthreads(); // the H_demag tile (x-inverse) is complete
+            while (valid) {
+                const int j = y0 + yl, i = 2 * ip;
                 const int f = z * sz + j * sy + i;
-                const bool xl = i > 0, xr = i + 2 < nx, ym = j > 0, yp = j + 1 < ny, zm = zg > 0,
-                           zp = zg + 1 < nzg;
                 float2 mc[3], ex[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const int q = c * csi + f;
-                    // a missing neighbour loads the centre's own address: every load is
-                    // unconditional and independent of the centre load (no select chain)
-                    const auto ld2 = [&](int o) { return __ldg(reinterpret_cast<const float2*>(m + o)); };
-                    const float2 ctr = ld2(q);
-                    float2 nb[6];
-                    nb[0] = make_float2(__ldg(m + (xl ? q - 1 : q)), ctr.x);
-                    nb[1] = make_float2(ctr.y, __ldg(m + (xr ? q + 2 : q + 1)));
-                    nb[2] = ld2(ym ? q - sy : q);
-                    nb[3] = ld2(yp ? q + sy : q);
-                    nb[4] = ld2(zm ? q - sz : q);
-                    nb[5] = ld2(zp ? q + sz : q);
-                    mc[c] = ctr;
-                    ex[c] = CellPairLLG::exch(ctr, nb);
+                    rn[c][0].y = rc[c].x; // the inner x neighbours are the pair's own centres
+                    rn[c][1].x = rc[c].y;
+                    mc[c] = rc[c];
+                    ex[c] = CellPairLLG::exch(rc[c], rn[c]);
                 }
+                // the next pair's loads go out before this pair's update
+                int yl2 = yl, ip2 = ip + NT;
+                while (ip2 >= nxh) {
+                    ip2 -= nxh;
+                    ++yl2;
+                }
+                const bool valid2 = yl2 < TR && y0 + yl2 < ny;
+                if (valid2) load_pair(yl2, ip2);
                 float2* hp = reinterpret_cast<float2*>(hm + yl * nx + i);
-                const int hc = (TR * nx) >> 1; // float2 stride between the component tiles
                 float2 hx = hp[0], hy = hp[hc], hz = hp[2 * hc];
                 pl.heff(mc[0], hx, hy, hz, ex[0], ex[1], ex[2]);
                 double t0, t1;
@@ -788,16 +806,15 @@ __global__ void __launch_bounds__(XS<LOG2L, PB, sizeof(T)>::NT, xs_min_blocks<T,
                     *reinterpret_cast<float2*>(mout + (c * csi + f)) = mc[c];
                     hp[c * hc] = mc[c];
                 }
-                ip += NT;
-                while (ip >= nxh) {
-                    ip -= nxh;
-                    ++yl;
-                }
+                yl = yl2;
+                ip = ip2;
+                valid = valid2;
             }
             goto llg_done;
         }
     }
 #endif
+    __syncthreads(); // the H_demag tile (x-inverse) is complete
     {
     // walk the tile's cells with a fixed stride, carrying (yl, i) instead of dividing
     int yl = 0, i = tid;
